@@ -1,0 +1,179 @@
+/* qtng.h -- C ABI of the B200 bucket-elimination contraction engine.
+ *
+ * This is the drop-in boundary for the reference's contraction hot path
+ * (/root/reference/proj, "qtnsim").  Plain pointers and sizes only; no C++
+ * or torch types.  Each entry point names the reference interface it
+ * replaces.  A C++ adaptor implementing qtnsim::ContractionBackend on top of
+ * qtng_contract_bucket ships as include/qtng_backend.hpp; INTEGRATION.md
+ * shows how a maintainer wires it into the reference's CLI/backend registry.
+ *
+ * Conventions (identical to the reference):
+ *   - complex numbers are complex128, interleaved (re, im) doubles
+ *     (proj/include/qtnsim/tensor.hpp:11,19);
+ *   - a tensor over binary variables is row-major in its var order, first
+ *     axis = most significant bit (tensor.hpp:13-15);
+ *   - bucket results have their axes in ascending variable id
+ *     (proj/include/qtnsim/engine.hpp:28-29); an empty result is a 1-element
+ *     scalar;
+ *   - graphs are edge lists of (u, v) int pairs; angles are p gammas and p
+ *     betas (proj/include/qtnsim/circuit.hpp:14-20).
+ *
+ * Every function returns a qtng_status; on failure qtng_last_error() holds
+ * the message, worded exactly like the reference's exception for the same
+ * condition.  Status codes map 1:1 onto the reference's exception types
+ * (proj/include/qtnsim/errors.hpp:8-36).
+ *
+ * Threading: a context serialises its device work internally, so one
+ * context may be shared by the reference's `jobs` worker threads
+ * (proj/src/engine.cpp:531-541).  Contexts on different devices are
+ * independent.
+ */
+#ifndef QTNG_H
+#define QTNG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum qtng_status {
+  QTNG_OK = 0,
+  QTNG_ERR_INVALID_INPUT = 1, /* qtnsim::InvalidInputError */
+  QTNG_ERR_RESOURCE = 2,      /* qtnsim::ResourceError     */
+  QTNG_ERR_SCHEDULE = 3,      /* qtnsim::ScheduleError     */
+  QTNG_ERR_NUMERICAL = 4,     /* qtnsim::NumericalError    */
+  QTNG_ERR_CUDA = 5,          /* device failure (no reference counterpart) */
+  QTNG_ERR_GENERATION = 6     /* qtnsim::GenerationError   */
+} qtng_status;
+
+typedef struct qtng_ctx qtng_ctx;
+typedef struct qtng_plan qtng_plan;
+
+/* One record per non-empty bucket, as TimingRecord (proj/include/qtnsim/engine.hpp:71-80).
+ * elapsed_s is the bucket's share (by algorithmic bytes) of its level's
+ * device time; backend is always "b200". */
+typedef struct qtng_record {
+  int32_t edge_u, edge_v;
+  int32_t bucket_seq;
+  int32_t width;
+  double elapsed_s;
+  uint64_t ops;     /* 2^width */
+  double flops_est; /* 8 * ops / elapsed_s */
+} qtng_record;
+
+typedef struct qtng_plan_info {
+  int32_t n_lightcones;
+  int32_t n_levels;          /* dependency levels = level_kernel launches */
+  uint64_t n_buckets;        /* non-empty buckets (= records) */
+  uint64_t n_device_ops;     /* bucket ops incl. pre-folds of >8-member buckets */
+  int32_t max_width;
+  int32_t max_result_rank;   /* peak_tensor_bytes = 16 << max_result_rank */
+  double alg_bytes;          /* sum over ops of 16*(sum_in 2^rank + 2^r) */
+  double sum_ops;            /* sum over buckets of 2^width */
+  uint64_t arena_bytes;      /* peak HBM arena footprint */
+  uint64_t desc_bytes;       /* descriptor bytes uploaded per plan */
+  int32_t kernels_per_run;   /* kernel launches per execution */
+} qtng_plan_info;
+
+/* ---------------------------------------------------------------- context */
+
+/* Create a context on CUDA `device`.  arena_bytes = initial HBM reservation
+ * (0 = grow on demand). */
+qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out);
+void qtng_destroy(qtng_ctx* ctx);
+/* Message of the calling thread's last failure ("" after success). */
+const char* qtng_last_error(void);
+/* Library build string (arch, version). */
+const char* qtng_version(void);
+
+/* ---------------------------------------------------------------- host side */
+
+/* random_regular (proj/src/graph.cpp:45-76): edges written to edges[2*m];
+ * *m_out = edge count.  cap = capacity in edges. */
+qtng_status qtng_random_regular(int n, int d, uint64_t seed, int* edges, int cap, int* m_out);
+
+/* edge_schedule (proj/src/engine.cpp:493-501) for edge `edge_index` of the
+ * sorted edge list, flattened as: per bucket n_sum, sum_vars, n_tensors,
+ * per tensor rank, vars; data = every tensor's entries (re, im) in the same
+ * order (the format of oracle/qtn_oracle.h).  *n_ints / *n_data receive the
+ * required sizes; nothing is written when a capacity is too small. */
+qtng_status qtng_edge_schedule(int n, int m, const int* edges, int p, const double* gammas,
+                               const double* betas, int edge_index, int merged, int* ints,
+                               int64_t int_cap, double* data, int64_t data_cap,
+                               int64_t* n_ints, int64_t* n_data, int* n_buckets);
+
+/* simulate_widths (proj/src/engine.cpp:235-240) of one edge's schedule. */
+qtng_status qtng_simulate_widths(int n, int m, const int* edges, int p, int edge_index,
+                                 int merged, int* widths, int cap, int* n_out);
+
+/* Predicted algorithmic bytes (SURVEY.md §8(a) B_alg) of every edge's
+ * lightcone: the load-balancing key for multi-GPU sharding. */
+qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged,
+                            double* bytes_out);
+
+/* ---------------------------------------------------------------- device side */
+
+/* ContractionBackend::contract (proj/include/qtnsim/engine.hpp:30;
+ * NaiveBackend::contract proj/src/engine.cpp:68-108): sum `sum_vars` out of
+ * the tensors.  ranks[t]; vars = concatenated var lists; data = concatenated
+ * tensors.  Host buffers in and out.  Result axes ascending. */
+qtng_status qtng_contract_bucket(qtng_ctx* ctx, int n_tensors, const int* ranks,
+                                 const int* vars, const double* data, int n_sum,
+                                 const int* sum_vars, int* out_rank, int* out_vars,
+                                 double* out_data, int64_t out_cap);
+
+/* contract_network (proj/src/engine.cpp:246-304) of one flattened schedule
+ * (format of qtng_edge_schedule), with contract_bucket's result-width cap
+ * (engine.cpp:160-169).  Records: up to rec_cap written, *n_records = count. */
+qtng_status qtng_contract_schedule(qtng_ctx* ctx, int n_buckets, const int* ints, int64_t n_ints,
+                                   const double* data, int max_result_width,
+                                   double* scalar_re_im, qtng_record* records, int rec_cap,
+                                   int* n_records, uint64_t* peak_tensor_bytes);
+
+/* energy_expectation (proj/src/engine.cpp:503-563): <C> = m/2 - 1/2 sum Re e_jk,
+ * all lightcones of the selected edges on this device in one level-batched
+ * program.  sel = NULL selects every edge; terms (may be NULL) receives
+ * 2*n_sel doubles (e_jk re, im) in selection order.  The energy is only
+ * meaningful when every edge is selected (it is m/2 - 1/2 sum over the
+ * selection otherwise). */
+qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
+                        const double* gammas, const double* betas, int merged,
+                        int max_result_width, int n_sel, const int* sel, double* energy,
+                        double* terms);
+
+/* ---------------------------------------------------------------- plans */
+
+/* Angle-independent plan of the selected edges' lightcones, uploaded to the
+ * device once; executions then take only the 2p angles. */
+qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int p, int merged,
+                             int max_result_width, int n_sel, const int* sel,
+                             qtng_plan** out);
+/* Run the plan for one angle set.  terms (host, may be NULL) receives
+ * 2*n_sel doubles.  device_ms (may be NULL) = device time of the kernels
+ * (CUDA events on the plan's stream). */
+qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const double* betas,
+                              double* terms, float* device_ms);
+/* Device-only re-execution with the current angles (no host copies), for
+ * throughput measurement; n_runs back-to-back runs, total device time. */
+qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms);
+qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info);
+/* Records of the last execution (edge_u/edge_v filled from the selection). */
+qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64_t cap,
+                              int64_t* n_out);
+/* Per-level device time of the last qtng_plan_execute (ms), n_levels entries. */
+qtng_status qtng_plan_level_ms(const qtng_plan* plan, float* ms, int cap);
+void qtng_plan_destroy(qtng_plan* plan);
+
+/* Largest-bucket microbenchmark support: time one level of the plan in
+ * isolation (the level containing the plan's widest bucket when level < 0).
+ * Returns the level index, its algorithmic bytes and the mean device ms over
+ * n_runs launches. */
+qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* level_out,
+                                 double* level_bytes, float* mean_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTNG_H */

@@ -1,0 +1,492 @@
+"""B200-native bucket-elimination contraction for QAOA MaxCut energies.
+
+A from-scratch sm_100a implementation of the hot path of the reference
+``qtnsim`` (arXiv 2204.06045's QTensor re-implementation, /root/reference/proj):
+the per-lightcone bucket elimination behind ``ContractionBackend`` /
+``contract_network`` / ``energy_expectation``.  This module mirrors that
+interface in Python (names, argument meaning and error types follow
+proj/include/qtnsim/*.hpp) on top of the C ABI in include/qtng.h; all compute
+runs in the native library ``libqtng.so`` (host planner in C++, kernels in
+CUDA for sm_100a).  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._native import PlanInfo, Record, lib
+
+__all__ = [
+    "InvalidInputError", "GenerationError", "ResourceError", "ScheduleError", "NumericalError",
+    "CudaError", "Graph", "Edge", "Angles", "Tensor", "Bucket", "ContractionSchedule",
+    "TimingRecord", "ContractionReport", "EnergyResult", "EngineConfig", "Context",
+    "GpuBackend", "Plan", "make_graph", "random_regular", "edge_schedule", "simulate_widths",
+    "edge_costs", "contract_bucket", "contract_network", "energy_expectation",
+    "default_context", "version",
+]
+
+
+# ------------------------------------------------------------------ errors
+# proj/include/qtnsim/errors.hpp:8-36
+class InvalidInputError(RuntimeError):
+    pass
+
+
+class GenerationError(RuntimeError):
+    pass
+
+
+class ResourceError(RuntimeError):
+    pass
+
+
+class ScheduleError(RuntimeError):
+    pass
+
+
+class NumericalError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERRORS = {1: InvalidInputError, 2: ResourceError, 3: ScheduleError, 4: NumericalError,
+           5: CudaError, 6: GenerationError}
+
+
+def _check(status: int) -> None:
+    if status:
+        raise _ERRORS.get(status, RuntimeError)(lib.qtng_last_error().decode())
+
+
+def version() -> str:
+    return lib.qtng_version().decode()
+
+
+# ------------------------------------------------------------------ graph
+@dataclass(frozen=True, order=True)
+class Edge:
+    u: int
+    v: int
+
+
+@dataclass
+class Graph:
+    """Undirected simple graph (graph.hpp:18-24); edges sorted, u < v."""
+
+    n: int
+    edges: np.ndarray  # (m, 2) int32
+
+    @property
+    def m(self) -> int:
+        return int(self.edges.shape[0])
+
+    def flat(self) -> np.ndarray:
+        return np.ascontiguousarray(self.edges.reshape(-1), dtype=np.int32)
+
+    def edge_list(self) -> List[Edge]:
+        return [Edge(int(u), int(v)) for u, v in self.edges]
+
+
+def make_graph(n: int, edges) -> Graph:
+    """make_graph (graph.cpp:30-43): normalise endpoint order, sort, reject
+    loops / out-of-range endpoints / duplicates."""
+    if n < 0:
+        raise InvalidInputError("vertex count must be non-negative")
+    es = []
+    for u, v in (tuple(e) for e in edges):
+        u, v = int(u), int(v)
+        if u > v:
+            u, v = v, u
+        if u == v:
+            raise InvalidInputError(f"self-loop at vertex {u}")
+        if u < 0 or v >= n:
+            raise InvalidInputError(f"edge endpoint out of range: ({u}, {v})")
+        es.append((u, v))
+    es.sort()
+    for a, b in zip(es, es[1:]):
+        if a == b:
+            raise InvalidInputError("duplicate edge")
+    arr = np.array(es, dtype=np.int32).reshape(-1, 2)
+    return Graph(n, arr)
+
+
+def random_regular(n: int, d: int, seed: int) -> Graph:
+    """random_regular (graph.cpp:45-76), identical edge set for a given seed."""
+    buf = np.zeros(max(2, n * max(d, 0) + 2), dtype=np.int32)
+    m = C.c_int(0)
+    _check(lib.qtng_random_regular(n, d, seed, buf, len(buf) // 2, C.byref(m)))
+    return Graph(n, buf[: 2 * m.value].reshape(-1, 2).copy())
+
+
+# ------------------------------------------------------------------ angles / config
+@dataclass
+class Angles:
+    """QAOA angles (circuit.hpp:14-20)."""
+
+    gammas: Sequence[float]
+    betas: Sequence[float]
+
+    def depth(self) -> int:
+        return len(self.gammas)
+
+    def validate(self) -> None:
+        if len(self.gammas) == 0 or len(self.gammas) != len(self.betas):
+            raise InvalidInputError("angles: gammas and betas must have equal length p >= 1")
+        if not all(np.isfinite(self.gammas)):
+            raise InvalidInputError("angles: non-finite gamma")
+        if not all(np.isfinite(self.betas)):
+            raise InvalidInputError("angles: non-finite beta")
+
+    def arrays(self):
+        return (np.ascontiguousarray(self.gammas, dtype=np.float64),
+                np.ascontiguousarray(self.betas, dtype=np.float64))
+
+
+@dataclass
+class EngineConfig:
+    """EngineConfig (engine.hpp:16-20)."""
+
+    max_result_width: int = 30
+
+    @staticmethod
+    def from_env() -> "EngineConfig":
+        cfg = EngineConfig()
+        v = os.environ.get("QTNSIM_MAX_WIDTH")
+        if v is not None:
+            try:
+                cfg.max_result_width = int(v)
+            except ValueError:
+                cfg.max_result_width = 0  # std::atoi semantics
+        return cfg
+
+
+# ------------------------------------------------------------------ tensors / schedules
+@dataclass
+class Tensor:
+    """Dense complex128 tensor over binary vars, first axis = MSB (tensor.hpp:13-25)."""
+
+    label: str
+    vars: List[int]
+    data: np.ndarray
+
+    def rank(self) -> int:
+        return len(self.vars)
+
+
+@dataclass
+class Bucket:
+    sum_vars: List[int]
+    tensors: List[Tensor] = field(default_factory=list)
+
+
+@dataclass
+class ContractionSchedule:
+    buckets: List[Bucket]
+    merges_applied: int = 0
+    merges_skipped: int = 0
+
+    def flatten(self):
+        ints: List[int] = []
+        data = []
+        for b in self.buckets:
+            ints.append(len(b.sum_vars))
+            ints.extend(int(v) for v in b.sum_vars)
+            ints.append(len(b.tensors))
+            for t in b.tensors:
+                ints.append(len(t.vars))
+                ints.extend(int(v) for v in t.vars)
+                data.append(np.ascontiguousarray(t.data, dtype=np.complex128).view(np.float64))
+        return (np.array(ints or [0], dtype=np.int32), len(ints),
+                np.concatenate(data) if data else np.zeros(2))
+
+
+@dataclass
+class TimingRecord:
+    """TimingRecord (engine.hpp:71-80)."""
+
+    edge_u: int
+    edge_v: int
+    bucket_seq: int
+    width: int
+    backend: str
+    elapsed_s: float
+    ops: int
+    flops_est: float
+
+
+@dataclass
+class ContractionReport:
+    scalar: complex
+    records: List[TimingRecord]
+    peak_tensor_bytes: int
+
+
+@dataclass
+class EnergyResult:
+    energy: float
+    terms: np.ndarray  # complex e_jk per edge (edge order)
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One CUDA device's stream, HBM arena and staging buffers (qtng_ctx)."""
+
+    def __init__(self, device: int = 0, arena_bytes: int = 0):
+        h = C.c_void_p()
+        _check(lib.qtng_create(device, arena_bytes, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.qtng_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = {}
+_ctx_lock = threading.Lock()
+
+
+def default_context(device: Optional[int] = None) -> Context:
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0")) if "LOCAL_RANK" in os.environ else 0
+    with _ctx_lock:
+        if device not in _default_ctx:
+            _default_ctx[device] = Context(device)
+        return _default_ctx[device]
+
+
+# ------------------------------------------------------------------ backend (drop-in)
+def contract_bucket(bucket: Bucket, ctx: Optional[Context] = None) -> Tensor:
+    """ContractionBackend::contract (engine.hpp:30) on the B200: sums
+    bucket.sum_vars out of bucket.tensors; result axes ascending."""
+    ctx = ctx or default_context()
+    ranks = np.array([len(t.vars) for t in bucket.tensors] or [0], dtype=np.int32)
+    vars_ = np.array([v for t in bucket.tensors for v in t.vars] or [0], dtype=np.int32)
+    data = (np.concatenate([np.ascontiguousarray(t.data, dtype=np.complex128).view(np.float64)
+                            for t in bucket.tensors]) if bucket.tensors else np.zeros(2))
+    allv = {v for t in bucket.tensors for v in t.vars}
+    cap = 1 << len(allv)
+    out_vars = np.zeros(max(len(allv), 1), dtype=np.int32)
+    out = np.zeros(2 * cap, dtype=np.float64)
+    sv = np.array(list(bucket.sum_vars) or [0], dtype=np.int32)
+    r = C.c_int(0)
+    _check(lib.qtng_contract_bucket(ctx.handle, len(bucket.tensors), ranks, vars_,
+                                    np.ascontiguousarray(data), len(bucket.sum_vars), sv,
+                                    C.byref(r), out_vars, out, cap))
+    k = r.value
+    return Tensor("bucket_result", [int(v) for v in out_vars[:k]],
+                  out[: 2 << k].view(np.complex128).copy())
+
+
+class GpuBackend:
+    """Drop-in for qtnsim::ContractionBackend (engine.hpp:22-31)."""
+
+    def __init__(self, ctx: Optional[Context] = None):
+        self._ctx = ctx
+
+    @property
+    def ctx(self) -> Context:
+        return self._ctx or default_context()
+
+    def name(self) -> str:
+        return "b200"
+
+    def select(self, width: int) -> "GpuBackend":
+        return self
+
+    def contract(self, bucket: Bucket) -> Tensor:
+        return contract_bucket(bucket, self.ctx)
+
+
+# ------------------------------------------------------------------ schedules
+def _angles_arrays(angles: Angles):
+    g, b = angles.arrays()
+    return g, b
+
+
+def edge_schedule(g: Graph, edge_index: int, angles: Angles,
+                  merged: bool = False) -> ContractionSchedule:
+    """edge_schedule (engine.cpp:493-501), built by the native host planner."""
+    gam, bet = _angles_arrays(angles)
+    n_ints, n_data, nb = C.c_int64(0), C.c_int64(0), C.c_int(0)
+    probe_i = np.zeros(1, np.int32)
+    probe_d = np.zeros(1, np.float64)
+    _check(lib.qtng_edge_schedule(g.n, g.m, g.flat(), angles.depth(), gam, bet, edge_index,
+                                  int(merged), probe_i, 0, probe_d, 0, C.byref(n_ints),
+                                  C.byref(n_data), C.byref(nb)))
+    ints = np.zeros(max(1, n_ints.value), np.int32)
+    data = np.zeros(max(1, n_data.value), np.float64)
+    _check(lib.qtng_edge_schedule(g.n, g.m, g.flat(), angles.depth(), gam, bet, edge_index,
+                                  int(merged), ints, len(ints), data, len(data),
+                                  C.byref(n_ints), C.byref(n_data), C.byref(nb)))
+    return _parse_flat(ints[: n_ints.value], data[: n_data.value], nb.value)
+
+
+def _parse_flat(ints, data, n_buckets) -> ContractionSchedule:
+    cd = data.view(np.complex128)
+    i = 0
+    off = 0
+    buckets = []
+    for _ in range(n_buckets):
+        ns = int(ints[i]); i += 1
+        sums = [int(x) for x in ints[i:i + ns]]; i += ns
+        nt = int(ints[i]); i += 1
+        ts = []
+        for _ in range(nt):
+            r = int(ints[i]); i += 1
+            vs = [int(x) for x in ints[i:i + r]]; i += r
+            ts.append(Tensor("t", vs, cd[off:off + (1 << r)].copy()))
+            off += 1 << r
+        buckets.append(Bucket(sums, ts))
+    return ContractionSchedule(buckets)
+
+
+def simulate_widths(g: Graph, edge_index: int, p: int, merged: bool = False) -> List[int]:
+    """simulate_widths (engine.cpp:235-240) of one edge's schedule."""
+    buf = np.zeros(1 << 16, dtype=np.int32)
+    n = C.c_int(0)
+    _check(lib.qtng_simulate_widths(g.n, g.m, g.flat(), p, edge_index, int(merged), buf,
+                                    len(buf), C.byref(n)))
+    return [int(x) for x in buf[: n.value]]
+
+
+def edge_costs(g: Graph, p: int, merged: bool = False) -> np.ndarray:
+    """Predicted algorithmic bytes per edge lightcone (sharding key)."""
+    out = np.zeros(max(1, g.m), dtype=np.float64)
+    _check(lib.qtng_edge_costs(g.n, g.m, g.flat(), p, int(merged), out))
+    return out[: g.m]
+
+
+def contract_network(schedule: ContractionSchedule, backend: Optional[GpuBackend] = None,
+                     cfg: Optional[EngineConfig] = None) -> ContractionReport:
+    """contract_network (engine.cpp:246-304) of a whole schedule on the device."""
+    ctx = (backend.ctx if backend is not None else default_context())
+    cfg = cfg or EngineConfig()
+    ints, n_ints, data = schedule.flatten()
+    n_b = len(schedule.buckets)
+    recs = (Record * max(1, n_b))()
+    nrec = C.c_int(0)
+    peak = C.c_uint64(0)
+    sc = np.zeros(2, np.float64)
+    _check(lib.qtng_contract_schedule(ctx.handle, n_b, ints, n_ints, np.ascontiguousarray(data),
+                                      cfg.max_result_width, sc, recs, len(recs), C.byref(nrec),
+                                      C.byref(peak)))
+    records = [TimingRecord(-1, -1, r.bucket_seq, r.width, "b200", r.elapsed_s, r.ops,
+                            r.flops_est) for r in recs[: nrec.value]]
+    return ContractionReport(complex(sc[0], sc[1]), records, peak.value)
+
+
+def energy_expectation(g: Graph, angles: Angles, backend: Optional[GpuBackend] = None,
+                       merged: bool = False, cfg: Optional[EngineConfig] = None,
+                       edges: Optional[Sequence[int]] = None) -> EnergyResult:
+    """energy_expectation (engine.cpp:503-563): <C> = |E|/2 - 1/2 sum_e Re e_jk,
+    every lightcone contracted on the device in one level-batched program."""
+    angles.validate()
+    ctx = backend.ctx if backend is not None else default_context()
+    cfg = cfg or EngineConfig()
+    gam, bet = _angles_arrays(angles)
+    sel = None if edges is None else np.ascontiguousarray(edges, dtype=np.int32)
+    k = g.m if sel is None else len(sel)
+    terms = np.zeros(2 * max(1, k), np.float64)
+    e = C.c_double(0)
+    _check(lib.qtng_energy(ctx.handle, g.n, g.m, g.flat(), angles.depth(), gam, bet, int(merged),
+                           cfg.max_result_width, k,
+                           None if sel is None else sel.ctypes.data_as(C.c_void_p),
+                           C.byref(e), terms))
+    return EnergyResult(e.value, terms[: 2 * k].view(np.complex128).copy())
+
+
+# ------------------------------------------------------------------ plans
+class Plan:
+    """An angle-independent, device-resident plan of a set of lightcones.
+
+    Build once per graph (host schedules, levels, arena placement, descriptor
+    upload); each ``execute(angles)`` uploads only the gate table."""
+
+    def __init__(self, g: Graph, p: int, merged: bool = False,
+                 cfg: Optional[EngineConfig] = None, edges: Optional[Sequence[int]] = None,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        cfg = cfg or EngineConfig()
+        self.graph = g
+        self.p = p
+        self.sel = (np.arange(g.m, dtype=np.int32) if edges is None
+                    else np.ascontiguousarray(edges, dtype=np.int32))
+        h = C.c_void_p()
+        _check(lib.qtng_plan_create(self.ctx.handle, g.n, g.m, g.flat(), p, int(merged),
+                                    cfg.max_result_width, len(self.sel),
+                                    self.sel.ctypes.data_as(C.c_void_p), C.byref(h)))
+        self._h = h
+        self.last_device_ms = 0.0
+
+    def info(self) -> PlanInfo:
+        inf = PlanInfo()
+        _check(lib.qtng_plan_info_get(self._h, C.byref(inf)))
+        return inf
+
+    def execute(self, angles: Angles) -> np.ndarray:
+        """Per-edge complex e_jk of the selected edges (selection order)."""
+        gam, bet = _angles_arrays(angles)
+        if len(gam) != self.p or len(bet) != self.p:
+            raise InvalidInputError("angles: gammas and betas must have equal length p >= 1")
+        out = np.zeros(2 * max(1, len(self.sel)), np.float64)
+        ms = C.c_float(0)
+        _check(lib.qtng_plan_execute(self._h, gam, bet, out.ctypes.data_as(C.c_void_p),
+                                     C.byref(ms)))
+        self.last_device_ms = ms.value
+        return out[: 2 * len(self.sel)].view(np.complex128).copy()
+
+    def run_device(self, n_runs: int = 1) -> float:
+        ms = C.c_float(0)
+        _check(lib.qtng_plan_run_device(self._h, n_runs, C.byref(ms)))
+        return ms.value
+
+    def level_ms(self) -> np.ndarray:
+        n = self.info().n_levels
+        out = np.zeros(max(1, n), np.float32)
+        _check(lib.qtng_plan_level_ms(self._h, out, n))
+        return out[:n]
+
+    def time_level(self, level: int = -1, n_runs: int = 10):
+        lv, by, ms = C.c_int(0), C.c_double(0), C.c_float(0)
+        _check(lib.qtng_plan_time_level(self._h, level, n_runs, C.byref(lv), C.byref(by),
+                                        C.byref(ms)))
+        return lv.value, by.value, ms.value
+
+    def records(self) -> List[TimingRecord]:
+        n = C.c_int64(0)
+        _check(lib.qtng_plan_records(self._h, None, 0, C.byref(n)))
+        recs = (Record * max(1, n.value))()
+        _check(lib.qtng_plan_records(self._h, recs, n.value, C.byref(n)))
+        return [TimingRecord(r.edge_u, r.edge_v, r.bucket_seq, r.width, "b200", r.elapsed_s,
+                             r.ops, r.flops_est) for r in recs[: n.value]]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.qtng_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,737 @@
+// C ABI (include/qtng.h): contexts, plans, and the orchestration of the
+// level-batched device program.
+#include "qtng.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "host.hpp"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace qtng;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define QTNG_CUDA(call)                                                                  \
+  do {                                                                                   \
+    const cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                               \
+      throw Error(kCuda, std::string(#call) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+template <class F>
+qtng_status guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return QTNG_OK;
+  } catch (const Error& ex) {
+    g_err = ex.what();
+    return static_cast<qtng_status>(ex.code);
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return QTNG_ERR_RESOURCE;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return QTNG_ERR_INVALID_INPUT;
+  }
+}
+
+// Growable device / pinned-host buffers.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n) {
+    if (n <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    QTNG_CUDA(cudaMalloc(&p, n));
+    cap = n;
+  }
+  ~DevBuf() { if (p) cudaFree(p); }
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n) {
+    if (n <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    QTNG_CUDA(cudaHostAlloc(&p, n, cudaHostAllocDefault));
+    cap = n;
+  }
+  ~PinBuf() { if (p) cudaFreeHost(p); }
+};
+
+Graph graph_from(int n, int m, const int* edges) {
+  if (m < 0 || (m > 0 && !edges)) throw Error(kInvalidInput, "edge list missing");
+  std::vector<Edge> es(m);
+  for (int i = 0; i < m; ++i) es[i] = Edge{edges[2 * i], edges[2 * i + 1]};
+  return make_graph(n, std::move(es));
+}
+
+void validate_angles(int p, const double* g, const double* b) {
+  // Angles::validate (proj/src/circuit.cpp:9-16)
+  if (p < 1 || !g || !b)
+    throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+  for (int k = 0; k < p; ++k)
+    if (!std::isfinite(g[k])) throw Error(kInvalidInput, "angles: non-finite gamma");
+  for (int k = 0; k < p; ++k)
+    if (!std::isfinite(b[k])) throw Error(kInvalidInput, "angles: non-finite beta");
+}
+
+std::vector<int> selection(int m, int n_sel, const int* sel) {
+  std::vector<int> s;
+  if (!sel) {
+    s.resize(m);
+    for (int i = 0; i < m; ++i) s[i] = i;
+    return s;
+  }
+  s.assign(sel, sel + n_sel);
+  for (int i : s)
+    if (i < 0 || i >= m) throw Error(kInvalidInput, "edge index out of range");
+  return s;
+}
+
+// Schedules + symbolic walks of the selected edges, built on host threads
+// (every lightcone is independent, like the reference's edge pool).
+struct ConeSet {
+  std::vector<WalkResult> walks;
+  std::vector<Edge> edges;
+};
+
+ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std::vector<int>& sel) {
+  ConeSet cs;
+  const int k = static_cast<int>(sel.size());
+  cs.walks.resize(k);
+  cs.edges.resize(k);
+  std::vector<std::string> errs(k);
+  std::vector<int> codes(k, 0);
+  auto work = [&](int i) {
+    try {
+      const Edge e = g.edges[sel[i]];
+      cs.edges[i] = e;
+      Schedule s = edge_schedule(g, e, p);
+      if (merged) s = merge_buckets(s);
+      cs.walks[i] = walk_schedule(s, max_width);
+    } catch (const Error& ex) {
+      codes[i] = ex.code;
+      errs[i] = ex.what();
+    }
+  };
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int nthreads = std::min(hw, k);
+  if (nthreads <= 1) {
+    for (int i = 0; i < k; ++i) work(i);
+  } else {
+    std::atomic<int> next{0};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nthreads; ++t)
+      pool.emplace_back([&] {
+        for (int i = next.fetch_add(1); i < k; i = next.fetch_add(1)) work(i);
+      });
+    for (auto& t : pool) t.join();
+  }
+  for (int i = 0; i < k; ++i)
+    if (codes[i]) throw Error(codes[i], errs[i]);
+  return cs;
+}
+
+// Descriptor image of a HostPlan: one contiguous blob, 256-byte aligned sections.
+struct DescLayout {
+  size_t ops = 0, trefs = 0, scal = 0, lcb = 0, terms = 0, total = 0;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t{255}; }
+
+DescLayout layout_of(const HostPlan& hp) {
+  DescLayout L;
+  size_t o = 0;
+  L.ops = o; o = align256(o + hp.ops.size() * sizeof(DevOp));
+  L.trefs = o; o = align256(o + hp.trefs.size() * sizeof(DevTensor));
+  L.scal = o; o = align256(o + hp.scalar_off.size() * sizeof(uint64_t));
+  L.lcb = o; o = align256(o + hp.lc_begin.size() * sizeof(uint32_t));
+  L.terms = o; o = align256(o + (hp.lc_begin.size()) * sizeof(double2));
+  L.total = o;
+  return L;
+}
+
+void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
+  std::memcpy(dst + L.ops, hp.ops.data(), hp.ops.size() * sizeof(DevOp));
+  std::memcpy(dst + L.trefs, hp.trefs.data(), hp.trefs.size() * sizeof(DevTensor));
+  std::memcpy(dst + L.scal, hp.scalar_off.data(), hp.scalar_off.size() * sizeof(uint64_t));
+  std::memcpy(dst + L.lcb, hp.lc_begin.data(), hp.lc_begin.size() * sizeof(uint32_t));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- context
+
+struct qtng_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DevBuf arena;          // double2 elements
+  uint64_t arena_gen = 0;
+  DevBuf desc;           // scratch descriptors (one-shot calls)
+  PinBuf pin_desc, pin_in, pin_out;
+  DevBuf flush;          // L2 flush scratch
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  void ensure_arena(uint64_t elems) {
+    const size_t bytes = std::max<uint64_t>(elems, 32) * sizeof(double2);
+    if (bytes > arena.cap) {
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      if (bytes > free_b + arena.cap)
+        throw Error(kResource, "device arena of " + std::to_string(bytes) +
+                                   " bytes exceeds free HBM (" + std::to_string(free_b) + ")");
+      arena.ensure(bytes);
+      ++arena_gen;
+    }
+  }
+  double2* A() { return static_cast<double2*>(arena.p); }
+};
+
+namespace {
+
+struct DevProgram {
+  char* base = nullptr;
+  DescLayout L;
+  const DevOp* ops() const { return reinterpret_cast<const DevOp*>(base + L.ops); }
+  const DevTensor* trefs() const { return reinterpret_cast<const DevTensor*>(base + L.trefs); }
+  const uint64_t* scal() const { return reinterpret_cast<const uint64_t*>(base + L.scal); }
+  const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
+  double2* terms() const { return reinterpret_cast<double2*>(base + L.terms); }
+};
+
+// Enqueue the whole program on `s`: every level, then the per-lightcone products.
+void enqueue_program(cudaStream_t s, const HostPlan& hp, const DevProgram& pr, double2* arena,
+                     std::vector<cudaEvent_t>* level_events) {
+  for (size_t L = 0; L < hp.levels.size(); ++L) {
+    if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
+    QTNG_CUDA(launch_level(s, pr.ops(), pr.trefs(), arena, hp.levels[L]));
+  }
+  if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
+  QTNG_CUDA(launch_final(s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
+                         arena, pr.terms()));
+}
+
+// Ops of the reference's run_edge post-processing (engine.cpp:517-519, 543-546).
+void check_terms(const std::vector<Edge>& edges, const double* terms) {
+  for (size_t i = 0; i < edges.size(); ++i)
+    if (std::abs(terms[2 * i + 1]) > 1e-8)
+      throw Error(kSchedule, "edge (" + std::to_string(edges[i].u) + ", " +
+                                 std::to_string(edges[i].v) +
+                                 "): edge term has non-real value: imag = " +
+                                 std::to_string(terms[2 * i + 1]));
+}
+
+}  // namespace
+
+struct qtng_plan {
+  qtng_ctx* ctx = nullptr;
+  HostPlan hp;
+  std::vector<Edge> edges;
+  int p = 0;
+  DevBuf desc;
+  DevProgram prog;
+  PinBuf pin_gate, pin_terms;
+  std::vector<cudaEvent_t> lev_ev;
+  std::vector<float> level_ms;
+  cudaGraphExec_t graph = nullptr;
+  uint64_t graph_gen = ~uint64_t{0};
+  ~qtng_plan() {
+    for (cudaEvent_t e : lev_ev) cudaEventDestroy(e);
+    if (graph) cudaGraphExecDestroy(graph);
+  }
+};
+
+extern "C" {
+
+const char* qtng_last_error(void) { return g_err.c_str(); }
+
+const char* qtng_version(void) {
+  return "qtng 0.1 (sm_100a level-batched bucket elimination, complex128, bit-exact naive order)";
+}
+
+qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalidInput, "null output pointer");
+    auto ctx = std::make_unique<qtng_ctx>();
+    ctx->device = device;
+    QTNG_CUDA(cudaSetDevice(device));
+    QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    QTNG_CUDA(cudaEventCreate(&ctx->ev0));
+    QTNG_CUDA(cudaEventCreate(&ctx->ev1));
+    if (arena_bytes) ctx->ensure_arena(arena_bytes / sizeof(double2));
+    *out = ctx.release();
+  });
+}
+
+void qtng_destroy(qtng_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  cudaStream_t s = ctx->stream;
+  delete ctx;  // frees the arena and staging buffers
+  if (s) cudaStreamDestroy(s);
+}
+
+qtng_status qtng_random_regular(int n, int d, uint64_t seed, int* edges, int cap, int* m_out) {
+  return guarded([&] {
+    const Graph g = random_regular(n, d, seed);
+    const int m = static_cast<int>(g.edges.size());
+    if (m_out) *m_out = m;
+    if (m > cap) throw Error(kInvalidInput, "edge buffer too small");
+    for (int i = 0; i < m; ++i) {
+      edges[2 * i] = g.edges[i].u;
+      edges[2 * i + 1] = g.edges[i].v;
+    }
+  });
+}
+
+qtng_status qtng_edge_schedule(int n, int m, const int* edges, int p, const double* gammas,
+                               const double* betas, int edge_index, int merged, int* ints,
+                               int64_t int_cap, double* data, int64_t data_cap,
+                               int64_t* n_ints, int64_t* n_data, int* n_buckets) {
+  return guarded([&] {
+    validate_angles(p, gammas, betas);
+    const Graph g = graph_from(n, m, edges);
+    if (edge_index < 0 || edge_index >= m) throw Error(kInvalidInput, "edge index out of range");
+    Schedule s = edge_schedule(g, g.edges[edge_index], p);
+    if (merged) s = merge_buckets(s);
+    std::vector<double> table(2 * kSlotElems * n_gate_slots(p));
+    fill_gate_table(p, gammas, betas, table.data());
+    std::vector<int> iv;
+    std::vector<double> dv;
+    flatten_schedule(s, table.data(), iv, dv);
+    *n_ints = static_cast<int64_t>(iv.size());
+    *n_data = static_cast<int64_t>(dv.size());
+    *n_buckets = static_cast<int>(s.buckets.size());
+    if (static_cast<int64_t>(iv.size()) <= int_cap && static_cast<int64_t>(dv.size()) <= data_cap) {
+      std::copy(iv.begin(), iv.end(), ints);
+      std::copy(dv.begin(), dv.end(), data);
+    }
+  });
+}
+
+qtng_status qtng_simulate_widths(int n, int m, const int* edges, int p, int edge_index,
+                                 int merged, int* widths, int cap, int* n_out) {
+  return guarded([&] {
+    const Graph g = graph_from(n, m, edges);
+    if (edge_index < 0 || edge_index >= m) throw Error(kInvalidInput, "edge index out of range");
+    Schedule s = edge_schedule(g, g.edges[edge_index], p);
+    if (merged) s = merge_buckets(s);
+    const std::vector<int> w = simulate_widths(s);
+    *n_out = static_cast<int>(w.size());
+    if (static_cast<int>(w.size()) > cap) throw Error(kInvalidInput, "width buffer too small");
+    std::copy(w.begin(), w.end(), widths);
+  });
+}
+
+qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged, double* bytes_out) {
+  return guarded([&] {
+    const Graph g = graph_from(n, m, edges);
+    const ConeSet cs = plan_cones(g, p, merged != 0, 1 << 20, selection(m, m, nullptr));
+    for (int i = 0; i < m; ++i) {
+      double b = 0;
+      for (const Op& op : cs.walks[i].ops) {
+        b += 16.0 * static_cast<double>(uint64_t{1} << op.out_vars.size());
+        for (const OpInput& in : op.inputs) b += 16.0 * static_cast<double>(uint64_t{1} << in.vars.size());
+      }
+      bytes_out[i] = b;
+    }
+  });
+}
+
+// ---------------------------------------------------------------- one-shot device calls
+
+namespace {
+
+// Run a single-"lightcone" program whose inputs are `input` (complex count
+// input_elems) and return the HostPlan (for record / output offsets).
+void run_program_once(qtng_ctx* ctx, const HostPlan& hp, const double* input,
+                      uint64_t input_elems, double2* terms_host) {
+  const DescLayout L = layout_of(hp);
+  ctx->ensure_arena(std::max(hp.arena_elems, input_elems));
+  ctx->desc.ensure(L.total);
+  ctx->pin_desc.ensure(L.total);
+  pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
+  ctx->pin_in.ensure(std::max<uint64_t>(input_elems, 1) * sizeof(double2));
+  std::memcpy(ctx->pin_in.p, input, input_elems * sizeof(double2));
+  QTNG_CUDA(cudaMemcpyAsync(ctx->A(), ctx->pin_in.p, input_elems * sizeof(double2),
+                            cudaMemcpyHostToDevice, ctx->stream));
+  QTNG_CUDA(cudaMemcpyAsync(ctx->desc.p, ctx->pin_desc.p, L.total, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  DevProgram pr{static_cast<char*>(ctx->desc.p), L};
+  enqueue_program(ctx->stream, hp, pr, ctx->A(), nullptr);
+  if (terms_host) {
+    const size_t nb = (hp.lc_begin.size() - 1) * sizeof(double2);
+    QTNG_CUDA(cudaMemcpyAsync(terms_host, pr.terms(), nb, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+}
+
+}  // namespace
+
+qtng_status qtng_contract_bucket(qtng_ctx* ctx, int n_tensors, const int* ranks, const int* vars,
+                                 const double* data, int n_sum, const int* sum_vars,
+                                 int* out_rank, int* out_vars, double* out_data,
+                                 int64_t out_cap) {
+  return guarded([&] {
+    if (!ctx) throw Error(kInvalidInput, "null context");
+    if (n_tensors < 0 || n_sum < 0) throw Error(kInvalidInput, "negative count");
+    Schedule s;
+    s.buckets.resize(1);
+    s.buckets[0].sum_vars.assign(sum_vars, sum_vars + n_sum);
+    int64_t dof = 0;
+    long vo = 0;
+    for (int t = 0; t < n_tensors; ++t) {
+      if (ranks[t] < 0 || ranks[t] > kMaxRank)
+        throw Error(kInvalidInput, "tensor rank out of range");
+      SchedTensor st;
+      st.vars.assign(vars + vo, vars + vo + ranks[t]);
+      vo += ranks[t];
+      st.data = dof;
+      dof += int64_t{1} << ranks[t];
+      s.buckets[0].tensors.push_back(t);
+      s.init.push_back(std::move(st));
+    }
+    if (n_tensors == 0) {  // empty product: NaiveBackend yields the scalar 1
+      if (n_sum > 0) throw Error(kSchedule, "bucket sums a variable absent from its tensors");
+      *out_rank = 0;
+      if (out_cap < 1) throw Error(kInvalidInput, "output buffer too small");
+      out_data[0] = 1.0;
+      out_data[1] = 0.0;
+      return;
+    }
+    const WalkResult w = walk_schedule(s, 1 << 20, /*route=*/false);
+    if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
+    const Op& op = w.ops[0];
+    const int r = static_cast<int>(op.out_vars.size());
+    if ((int64_t{1} << r) > out_cap) throw Error(kInvalidInput, "output buffer too small");
+    const HostPlan hp = build_plan({&w}, static_cast<uint64_t>(dof));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    run_program_once(ctx, hp, data, static_cast<uint64_t>(dof), nullptr);
+    QTNG_CUDA(cudaMemcpyAsync(out_data, ctx->A() + hp.rec_out[0],
+                              (size_t{1} << r) * sizeof(double2), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out_rank = r;
+    std::copy(op.out_vars.begin(), op.out_vars.end(), out_vars);
+  });
+}
+
+qtng_status qtng_contract_schedule(qtng_ctx* ctx, int n_buckets, const int* ints, int64_t n_ints,
+                                   const double* data, int max_result_width,
+                                   double* scalar_re_im, qtng_record* records, int rec_cap,
+                                   int* n_records, uint64_t* peak_tensor_bytes) {
+  return guarded([&] {
+    if (!ctx) throw Error(kInvalidInput, "null context");
+    const Schedule s = parse_schedule(n_buckets, ints, static_cast<long>(n_ints));
+    const WalkResult w = walk_schedule(s, max_result_width);
+    if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
+    uint64_t input_elems = 0;
+    for (const SchedTensor& t : s.init) input_elems += uint64_t{1} << t.vars.size();
+    double2 scalar = make_double2(1.0, 0.0);
+    float ms = 0.f;
+    HostPlan hp;
+    if (!w.ops.empty()) {
+      hp = build_plan({&w}, input_elems);
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      QTNG_CUDA(cudaSetDevice(ctx->device));
+      QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+      run_program_once(ctx, hp, data, input_elems, &scalar);
+      QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+      QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+      QTNG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    }
+    scalar_re_im[0] = scalar.x;
+    scalar_re_im[1] = scalar.y;
+    const int n = static_cast<int>(w.ops.size());
+    if (n_records) *n_records = n;
+    double total_bytes = 0;
+    for (double b : hp.rec_bytes) total_bytes += b;
+    for (int i = 0; i < n && i < rec_cap && records; ++i) {
+      qtng_record& r = records[i];
+      r.edge_u = r.edge_v = -1;
+      r.bucket_seq = w.ops[i].bucket_seq;
+      r.width = w.ops[i].width;
+      r.ops = uint64_t{1} << r.width;
+      r.elapsed_s = std::max(1e-9, 1e-3 * ms * (total_bytes > 0 ? hp.rec_bytes[i] / total_bytes : 0));
+      r.flops_est = 8.0 * static_cast<double>(r.ops) / r.elapsed_s;
+    }
+    if (peak_tensor_bytes) *peak_tensor_bytes = w.ops.empty() ? 0 : (uint64_t{16} << w.max_result_rank);
+  });
+}
+
+// ---------------------------------------------------------------- plans
+
+qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int p, int merged,
+                             int max_result_width, int n_sel, const int* sel, qtng_plan** out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error(kInvalidInput, "null argument");
+    if (p < 1) throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+    const Graph g = graph_from(n, m, edges);
+    const std::vector<int> s = selection(m, n_sel, sel);
+    ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, s);
+    for (size_t i = 0; i < cs.walks.size(); ++i)
+      if (cs.walks[i].fail_code)
+        throw Error(kSchedule, "edge (" + std::to_string(cs.edges[i].u) + ", " +
+                                   std::to_string(cs.edges[i].v) + "): " + cs.walks[i].fail_msg);
+    auto plan = std::make_unique<qtng_plan>();
+    plan->ctx = ctx;
+    plan->p = p;
+    plan->edges = cs.edges;
+    std::vector<const WalkResult*> ptrs;
+    for (const WalkResult& w : cs.walks) ptrs.push_back(&w);
+    plan->hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems);
+    const HostPlan& hp = plan->hp;
+    const DescLayout L = layout_of(hp);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    plan->desc.ensure(L.total);
+    plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L};
+    ctx->pin_desc.ensure(L.total);
+    pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
+    QTNG_CUDA(cudaMemcpyAsync(plan->desc.p, ctx->pin_desc.p, L.total, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    plan->pin_gate.ensure(hp.input_elems * sizeof(double2));
+    plan->pin_terms.ensure(std::max<size_t>(1, cs.walks.size()) * sizeof(double2));
+    plan->lev_ev.resize(hp.levels.size() + 1);
+    for (cudaEvent_t& e : plan->lev_ev) QTNG_CUDA(cudaEventCreate(&e));
+    plan->level_ms.assign(hp.levels.size(), 0.f);
+    *out = plan.release();
+  });
+}
+
+qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const double* betas,
+                              double* terms, float* device_ms) {
+  return guarded([&] {
+    if (!plan) throw Error(kInvalidInput, "null plan");
+    validate_angles(plan->p, gammas, betas);
+    qtng_ctx* ctx = plan->ctx;
+    const HostPlan& hp = plan->hp;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    ctx->ensure_arena(hp.arena_elems);
+    fill_gate_table(plan->p, gammas, betas, static_cast<double*>(plan->pin_gate.p));
+    QTNG_CUDA(cudaMemcpyAsync(ctx->A(), plan->pin_gate.p, hp.input_elems * sizeof(double2),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    enqueue_program(ctx->stream, hp, plan->prog, ctx->A(), &plan->lev_ev);
+    QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    const size_t nb = plan->edges.size() * sizeof(double2);
+    QTNG_CUDA(cudaMemcpyAsync(plan->pin_terms.p, plan->prog.terms(), nb, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    QTNG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    for (size_t L = 0; L < hp.levels.size(); ++L)
+      QTNG_CUDA(cudaEventElapsedTime(&plan->level_ms[L], plan->lev_ev[L], plan->lev_ev[L + 1]));
+    if (device_ms) *device_ms = ms;
+    const double* t = static_cast<const double*>(plan->pin_terms.p);
+    if (terms) std::memcpy(terms, t, nb);
+    check_terms(plan->edges, t);
+  });
+}
+
+qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms) {
+  return guarded([&] {
+    if (!plan) throw Error(kInvalidInput, "null plan");
+    qtng_ctx* ctx = plan->ctx;
+    const HostPlan& hp = plan->hp;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    ctx->ensure_arena(hp.arena_elems);
+    if (!plan->graph || plan->graph_gen != ctx->arena_gen) {
+      if (plan->graph) cudaGraphExecDestroy(plan->graph);
+      plan->graph = nullptr;
+      cudaGraph_t gr = nullptr;
+      QTNG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      enqueue_program(ctx->stream, hp, plan->prog, ctx->A(), nullptr);
+      QTNG_CUDA(cudaStreamEndCapture(ctx->stream, &gr));
+      QTNG_CUDA(cudaGraphInstantiate(&plan->graph, gr, 0));
+      cudaGraphDestroy(gr);
+      plan->graph_gen = ctx->arena_gen;
+    }
+    QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    for (int i = 0; i < n_runs; ++i) QTNG_CUDA(cudaGraphLaunch(plan->graph, ctx->stream));
+    QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    QTNG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    if (device_ms) *device_ms = ms;
+  });
+}
+
+qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info) {
+  return guarded([&] {
+    if (!plan || !info) throw Error(kInvalidInput, "null argument");
+    const HostPlan& hp = plan->hp;
+    info->n_lightcones = static_cast<int32_t>(plan->edges.size());
+    info->n_levels = static_cast<int32_t>(hp.levels.size());
+    info->n_buckets = hp.n_buckets;
+    info->n_device_ops = hp.ops.size();
+    info->max_width = hp.max_width;
+    info->max_result_rank = hp.max_result_rank;
+    info->alg_bytes = hp.alg_bytes;
+    info->sum_ops = hp.sum_ops;
+    info->arena_bytes = hp.arena_elems * sizeof(double2);
+    info->desc_bytes = plan->prog.L.total;
+    info->kernels_per_run = kernels_per_plan(static_cast<int>(hp.levels.size()));
+  });
+}
+
+qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64_t cap,
+                              int64_t* n_out) {
+  return guarded([&] {
+    if (!plan) throw Error(kInvalidInput, "null plan");
+    const HostPlan& hp = plan->hp;
+    const int64_t n = static_cast<int64_t>(hp.rec_seq.size());
+    if (n_out) *n_out = n;
+    for (size_t c = 0; c + 1 < hp.rec_begin.size(); ++c)
+      for (uint32_t i = hp.rec_begin[c]; i < hp.rec_begin[c + 1] && i < cap; ++i) {
+        qtng_record& r = records[i];
+        r.edge_u = plan->edges[c].u;
+        r.edge_v = plan->edges[c].v;
+        r.bucket_seq = hp.rec_seq[i];
+        r.width = hp.rec_width[i];
+        r.ops = uint64_t{1} << r.width;
+        const int L = hp.rec_level[i];
+        const double share = hp.level_bytes[L] > 0 ? hp.rec_bytes[i] / hp.level_bytes[L] : 0;
+        r.elapsed_s = std::max(1e-9, 1e-3 * plan->level_ms[L] * share);
+        r.flops_est = 8.0 * static_cast<double>(r.ops) / r.elapsed_s;
+      }
+  });
+}
+
+qtng_status qtng_plan_level_ms(const qtng_plan* plan, float* ms, int cap) {
+  return guarded([&] {
+    if (!plan) throw Error(kInvalidInput, "null plan");
+    for (int i = 0; i < cap && i < static_cast<int>(plan->level_ms.size()); ++i) ms[i] = plan->level_ms[i];
+  });
+}
+
+void qtng_plan_destroy(qtng_plan* plan) {
+  if (!plan) return;
+  std::lock_guard<std::mutex> lk(plan->ctx->mu);
+  cudaSetDevice(plan->ctx->device);
+  delete plan;
+}
+
+qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* level_out,
+                                 double* level_bytes, float* mean_ms) {
+  return guarded([&] {
+    if (!plan) throw Error(kInvalidInput, "null plan");
+    const HostPlan& hp = plan->hp;
+    if (hp.levels.empty()) throw Error(kInvalidInput, "empty plan");
+    if (level < 0) {  // the level holding the widest bucket
+      int best = 0;
+      for (size_t i = 0; i < hp.rec_width.size(); ++i)
+        if (hp.rec_width[i] > hp.rec_width[best]) best = static_cast<int>(i);
+      level = hp.rec_level[best];
+    }
+    if (level >= static_cast<int>(hp.levels.size())) throw Error(kInvalidInput, "level out of range");
+    qtng_ctx* ctx = plan->ctx;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    ctx->ensure_arena(hp.arena_elems);
+    QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.trefs(), ctx->A(),
+                           hp.levels[level]));  // warm-up
+    QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    for (int i = 0; i < n_runs; ++i)
+      QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.trefs(), ctx->A(),
+                             hp.levels[level]));
+    QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    QTNG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    *level_out = level;
+    *level_bytes = hp.level_bytes[level];
+    *mean_ms = ms / std::max(1, n_runs);
+  });
+}
+
+// ---------------------------------------------------------------- energy (end to end)
+
+qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
+                        const double* gammas, const double* betas, int merged,
+                        int max_result_width, int n_sel, const int* sel, double* energy,
+                        double* terms) {
+  return guarded([&] {
+    if (!ctx) throw Error(kInvalidInput, "null context");
+    validate_angles(p, gammas, betas);
+    const Graph g = graph_from(n, m, edges);
+    const std::vector<int> s = selection(m, n_sel, sel);
+    ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, s);
+    // cap refusals surface per edge, the first in edge order wins (engine.cpp:543-546)
+    std::vector<const WalkResult*> ok;
+    std::vector<int> ok_idx;
+    int first_fail = -1;
+    for (size_t i = 0; i < cs.walks.size(); ++i) {
+      if (cs.walks[i].fail_code) {
+        if (first_fail < 0) first_fail = static_cast<int>(i);
+      } else {
+        ok.push_back(&cs.walks[i]);
+        ok_idx.push_back(static_cast<int>(i));
+      }
+    }
+    std::vector<double> t(2 * cs.walks.size(), 0.0);
+    if (!ok.empty()) {
+      const HostPlan hp = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems);
+      std::vector<double> table(2 * hp.input_elems);
+      fill_gate_table(p, gammas, betas, table.data());
+      std::vector<double2> tt(ok.size());
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      QTNG_CUDA(cudaSetDevice(ctx->device));
+      run_program_once(ctx, hp, table.data(), hp.input_elems, nullptr);
+      ctx->pin_out.ensure(ok.size() * sizeof(double2));
+      DevProgram pr{static_cast<char*>(ctx->desc.p), layout_of(hp)};
+      QTNG_CUDA(cudaMemcpyAsync(ctx->pin_out.p, pr.terms(), ok.size() * sizeof(double2),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+      const double* o = static_cast<const double*>(ctx->pin_out.p);
+      for (size_t k = 0; k < ok.size(); ++k) {
+        t[2 * ok_idx[k]] = o[2 * k];
+        t[2 * ok_idx[k] + 1] = o[2 * k + 1];
+      }
+    }
+    for (size_t i = 0; i < cs.walks.size(); ++i) {
+      const bool refused = cs.walks[i].fail_code != 0;
+      const bool complex_term = !refused && std::abs(t[2 * i + 1]) > 1e-8;
+      if (refused || complex_term) {
+        const std::string what = refused ? cs.walks[i].fail_msg
+                                         : "edge term has non-real value: imag = " +
+                                               std::to_string(t[2 * i + 1]);
+        throw Error(kSchedule, "edge (" + std::to_string(cs.edges[i].u) + ", " +
+                                   std::to_string(cs.edges[i].v) + "): " + what);
+      }
+    }
+    double sum = 0.0;  // edge order, like engine.cpp:549-551
+    for (size_t i = 0; i < cs.walks.size(); ++i) sum += t[2 * i];
+    if (energy) *energy = 0.5 * static_cast<double>(m) - 0.5 * sum;
+    if (terms) std::copy(t.begin(), t.end(), terms);
+  });
+}
+
+}  // extern "C"

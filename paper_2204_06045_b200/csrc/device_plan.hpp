@@ -1,0 +1,58 @@
+// Device-side descriptors of a planned elimination, shared by the host planner
+// (plan.cpp) and the sm_100a kernels (kernels.cu).
+//
+// HBM layout (one arena per context, complex128 = double2 elements):
+//   [0, input_elems)          input region: the gate table of the current angle
+//                             set (QAOA plans) or the uploaded initial tensors
+//                             (explicit schedules / single buckets)
+//   [input_elems, arena_elems) bucket results, placed by an offline best-fit
+//                             allocator over their level lifetimes (a result
+//                             lives from its producing level to its consuming
+//                             level), 512-byte aligned
+// Descriptors live in a separate device buffer owned by the plan.
+#pragma once
+
+#include <cstdint>
+
+namespace qtng {
+
+constexpr int kMaxInputs = 8;     // tensors per op (wider buckets are pre-folded)
+constexpr int kMaxRank = 32;      // axes per input tensor (offsets are 32-bit)
+constexpr int kMaxSumBits = 10;   // summed vars per op (merged buckets: <= 9 seen)
+constexpr int kItemBits = 10;     // outputs per warp work item = 2^min(r, kItemBits)
+constexpr uint8_t kSumSrc = 64;   // DevTensor::src >= kSumSrc: a summed bit
+
+// One bucket contraction: out[k] = sum_s prod_t in_t[gather_t(k, s)].
+// k runs MSB-first over the ascending kept vars, s MSB-first over the
+// ascending summed vars (so s ascending == the reference's accumulation order).
+struct alignas(16) DevOp {
+  uint64_t out;         // arena element offset of the result
+  uint32_t item_begin;  // first work item of this op inside its level
+  uint32_t tref;        // index of the op's first DevTensor
+  uint8_t r;            // result rank
+  uint8_t ns;           // summed bits
+  uint8_t nt;           // inputs (1..kMaxInputs), in bucket member order
+  uint8_t cb;           // log2(outputs per work item) = min(r, kItemBits)
+  uint32_t pad;
+};
+static_assert(sizeof(DevOp) == 32, "DevOp layout");
+
+// An input operand: its arena offset and, per axis (MSB first), where the
+// axis bit comes from -- output bit j (LSB-indexed) or summed bit kSumSrc+j.
+struct alignas(16) DevTensor {
+  uint64_t off;
+  uint8_t rank;
+  uint8_t src[kMaxRank + 7];
+};
+static_assert(sizeof(DevTensor) == 48, "DevTensor layout");
+
+// One level of the level-synchronous schedule: ops [op_begin, op_begin+op_count)
+// of the level-sorted op array, `items` warp work items in total.
+struct LevelLaunch {
+  uint32_t op_begin;
+  uint32_t op_count;
+  uint32_t items;
+  uint32_t pad;
+};
+
+}  // namespace qtng

@@ -1,0 +1,234 @@
+// sm_100a kernels of the bucket-elimination path.
+//
+// level_kernel -- the generic fused bucket kernel.  One launch runs every
+// bucket of one dependency level of ALL planned lightcones (tiny buckets cost
+// no launch of their own).  The unit of work is a warp "item": 2^min(r,10)
+// consecutive outputs of one bucket.  Per item each lane
+//   * decodes, once, every operand's bit-gather map into two 32-bit partial
+//     offsets: `lo` for its own output bits 0..4 and `hi` for output bits >= 5
+//     of the item row it will later broadcast (offsets are additive over bits
+//     because every output/sum bit maps to a distinct operand bit),
+//   * then walks the item's 2^(cb-5) rows: operand offset = lo + shfl(hi, row),
+//     128-bit read-only loads of complex128, product over operands in bucket
+//     member order, accumulation over the summed assignments in ascending
+//     order, one 128-bit store per output.
+// Operands that are sorted (every intermediate result) map their low bits to
+// the bucket's low output bits, so lanes read contiguous 16-byte elements;
+// the rank<=2 gate operands are L1-resident.  Products are rounded exactly as
+// the reference's std::complex<double> `prod *= x` (ac-bd, ad+bc, no FMA), so
+// results are bit-identical to its NaiveBackend (proj/src/engine.cpp:94-106).
+#include "kernels.cuh"
+
+#include <cstdint>
+
+namespace qtng {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  // (a.x*b.x - a.y*b.y, a.x*b.y + a.y*b.x), every product rounded.
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+
+__device__ __forceinline__ double2 ld(const double2* p) { return __ldg(p); }
+
+// NSM: 0 => no summed bit, 1 => one summed bit, 2 => 2..kMaxSumBits.
+template <int T, int NSM>
+__device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
+                                         const DevTensor* __restrict__ trefs,
+                                         double2* __restrict__ arena, int lane,
+                                         DevTensor* slot) {
+  const int cb = op.cb;
+  const uint64_t kbase = static_cast<uint64_t>(chunk) << cb;
+  const bool active = cb >= 5 || lane < (1 << cb);
+  const uint32_t my = active ? lane : 0;
+  const uint64_t khi = kbase | (static_cast<uint64_t>(lane) << 5);  // lane = row for `hi`
+  // Stage the op's operand descriptors in this warp's shared slot; the
+  // per-axis decode below then reads its source bits with broadcast LDS.
+  {
+    const uint4* src4 = reinterpret_cast<const uint4*>(trefs + op.tref);
+    uint4* dst4 = reinterpret_cast<uint4*>(slot);
+    if (lane < 3 * T) dst4[lane] = __ldg(src4 + lane);
+    __syncwarp();
+  }
+  const double2* base[T];
+  uint32_t lo[T], hi[T], sa[T], sb[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const DevTensor& d = slot[t];
+    base[t] = arena + d.off;
+    const int rank = d.rank;
+    uint32_t l = 0, h = 0, a = 0, b = 0;
+#pragma unroll 1
+    for (int ax = 0; ax < rank; ++ax) {
+      const uint32_t src = d.src[ax];
+      const uint32_t bit = 1u << (rank - 1 - ax);
+      if (src < 5) {
+        l |= ((my >> src) & 1u) ? bit : 0u;
+      } else if (src < kSumSrc) {
+        h |= ((khi >> src) & 1u) ? bit : 0u;
+      } else {
+        const uint32_t j = src - kSumSrc;
+        if (NSM == 1) {
+          a |= bit;
+        } else if (j < 5) {
+          a |= ((static_cast<uint32_t>(lane) >> j) & 1u) ? bit : 0u;
+        } else {
+          b |= ((static_cast<uint32_t>(lane) >> (j - 5)) & 1u) ? bit : 0u;
+        }
+      }
+    }
+    lo[t] = l;
+    hi[t] = h;
+    sa[t] = a;
+    sb[t] = b;
+  }
+  __syncwarp();  // the slot is rewritten by the warp's next item
+  const int rows = cb > 5 ? 1 << (cb - 5) : 1;
+  double2* out = arena + op.out + kbase + my;
+  const int ns = op.ns;
+#pragma unroll 2
+  for (int e = 0; e < rows; ++e) {
+    uint32_t off[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) off[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
+    double2 acc = make_double2(0.0, 0.0);
+    if (NSM == 0) {
+      double2 prod = make_double2(1.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < T; ++t) prod = cmul(prod, ld(base[t] + off[t]));
+      acc = cadd(acc, prod);
+    } else if (NSM == 1) {
+      double2 x0[T], x1[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        x0[t] = ld(base[t] + off[t]);
+        x1[t] = ld(base[t] + off[t] + sa[t]);
+      }
+      double2 p0 = make_double2(1.0, 0.0), p1 = make_double2(1.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        p0 = cmul(p0, x0[t]);
+        p1 = cmul(p1, x1[t]);
+      }
+      acc = cadd(cadd(acc, p0), p1);
+    } else {
+      const int n_hi = ns > 5 ? 1 << (ns - 5) : 1;
+      const int n_lo = ns > 5 ? 32 : 1 << ns;
+      for (int sh = 0; sh < n_hi; ++sh) {
+        uint32_t offh[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) offh[t] = off[t] + __shfl_sync(kFull, sb[t], sh);
+        for (int sl = 0; sl < n_lo; ++sl) {
+          double2 prod = make_double2(1.0, 0.0);
+#pragma unroll
+          for (int t = 0; t < T; ++t)
+            prod = cmul(prod, ld(base[t] + offh[t] + __shfl_sync(kFull, sa[t], sl)));
+          acc = cadd(acc, prod);
+        }
+      }
+    }
+    if (active) out[static_cast<uint64_t>(e) << 5] = acc;
+  }
+}
+
+template <int T>
+__device__ __forceinline__ void dispatch_ns(const DevOp& op, uint32_t chunk,
+                                            const DevTensor* __restrict__ trefs,
+                                            double2* __restrict__ arena, int lane,
+                                            DevTensor* slot) {
+  if (op.ns == 1) run_item<T, 1>(op, chunk, trefs, arena, lane, slot);
+  else if (op.ns == 0) run_item<T, 0>(op, chunk, trefs, arena, lane, slot);
+  else run_item<T, 2>(op, chunk, trefs, arena, lane, slot);
+}
+
+__global__ void __launch_bounds__(kThreads)
+level_kernel(const DevOp* __restrict__ ops, const DevTensor* __restrict__ trefs,
+             double2* __restrict__ arena, uint32_t op_count, uint32_t items) {
+  __shared__ DevTensor slots[kWarpsPerCta][kMaxInputs];
+  const int lane = threadIdx.x & 31;
+  DevTensor* slot = slots[threadIdx.x >> 5];
+  const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  uint32_t cur = 0, cur_begin = 1, cur_end = 0;  // cached op lookup
+  for (uint32_t item = warp; item < items; item += nwarps) {
+    if (item < cur_begin || item >= cur_end) {
+      uint32_t lo = 0, hi = op_count;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&ops[mid].item_begin) <= item) lo = mid; else hi = mid;
+      }
+      cur = lo;
+      cur_begin = __ldg(&ops[lo].item_begin);
+      cur_end = lo + 1 < op_count ? __ldg(&ops[lo + 1].item_begin) : items;
+    }
+    const DevOp op = ops[cur];
+    const uint32_t chunk = item - cur_begin;
+    switch (op.nt) {
+      case 1: dispatch_ns<1>(op, chunk, trefs, arena, lane, slot); break;
+      case 2: dispatch_ns<2>(op, chunk, trefs, arena, lane, slot); break;
+      case 3: dispatch_ns<3>(op, chunk, trefs, arena, lane, slot); break;
+      case 4: dispatch_ns<4>(op, chunk, trefs, arena, lane, slot); break;
+      case 5: dispatch_ns<5>(op, chunk, trefs, arena, lane, slot); break;
+      case 6: dispatch_ns<6>(op, chunk, trefs, arena, lane, slot); break;
+      case 7: dispatch_ns<7>(op, chunk, trefs, arena, lane, slot); break;
+      default: dispatch_ns<8>(op, chunk, trefs, arena, lane, slot); break;
+    }
+  }
+}
+
+__global__ void final_kernel(const uint64_t* __restrict__ scalar_off,
+                             const uint32_t* __restrict__ lc_begin, int n_lc,
+                             const double2* __restrict__ arena, double2* __restrict__ terms) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_lc) return;
+  double2 s = make_double2(1.0, 0.0);  // report.scalar = 1 (engine.cpp:253)
+  for (uint32_t k = lc_begin[i]; k < lc_begin[i + 1]; ++k) s = cmul(s, arena[scalar_off[k]]);
+  terms[i] = s;
+}
+
+int resident_ctas() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_kernel, kThreads, 0);
+    cached = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return cached;
+}
+
+}  // namespace
+
+int level_grid(uint32_t items) {
+  const uint32_t want = (items + kWarpsPerCta - 1) / kWarpsPerCta;
+  const uint32_t cap = static_cast<uint32_t>(resident_ctas());
+  return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const DevTensor* trefs,
+                         double2* arena, const LevelLaunch& lv) {
+  if (lv.items == 0) return cudaSuccess;
+  level_kernel<<<level_grid(lv.items), kThreads, 0, s>>>(ops + lv.op_begin, trefs, arena,
+                                                        lv.op_count, lv.items);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint32_t* lc_begin,
+                         int n_lc, const double2* arena, double2* terms) {
+  if (n_lc <= 0) return cudaSuccess;
+  final_kernel<<<(n_lc + 127) / 128, 128, 0, s>>>(scalar_off, lc_begin, n_lc, arena, terms);
+  return cudaGetLastError();
+}
+
+}  // namespace qtng

@@ -1,0 +1,25 @@
+// Launch interface of the sm_100a bucket kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device_plan.hpp"
+
+namespace qtng {
+
+// Number of CTAs (256 threads) a level launch with `items` warp work items
+// uses: enough for one item per warp, capped at the resident CTA count.
+int level_grid(uint32_t items);
+
+// One level: every op of the level, all lightcones at once.
+cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const DevTensor* trefs,
+                         double2* arena, const LevelLaunch& lv);
+
+// Per lightcone: e_jk = prod of its scalar results in production order.
+cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint32_t* lc_begin,
+                         int n_lc, const double2* arena, double2* terms);
+
+// Number of kernels launched per plan execution (levels + final).
+inline int kernels_per_plan(int n_levels) { return n_levels + 1; }
+
+}  // namespace qtng

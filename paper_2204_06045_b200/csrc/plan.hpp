@@ -1,0 +1,41 @@
+// Offline planning of a batch of lightcone eliminations for one device:
+// level assignment across all lightcones, HBM arena placement, and the flat
+// descriptor arrays the kernels consume.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "device_plan.hpp"
+#include "host.hpp"
+
+namespace qtng {
+
+struct HostPlan {
+  std::vector<DevOp> ops;              // level-sorted
+  std::vector<DevTensor> trefs;
+  std::vector<LevelLaunch> levels;
+  std::vector<uint64_t> scalar_off;    // per lightcone: its scalar results, production order
+  std::vector<uint32_t> lc_begin;      // n_lightcones + 1 prefix into scalar_off
+  uint64_t input_elems = 0;
+  uint64_t arena_elems = 0;            // peak arena size (elements)
+  // accounting: B_alg = sum_in 16*2^rank + 16*2^r; ops = 2^width
+  double alg_bytes = 0;
+  double sum_ops = 0;
+  std::vector<double> level_bytes;     // B_alg per level
+  uint64_t n_buckets = 0;              // non-empty buckets (= TimingRecords)
+  int max_width = 0;
+  int max_result_rank = 0;
+  // per lightcone record data (one per non-empty bucket, schedule order)
+  std::vector<uint32_t> rec_begin;     // n_lightcones + 1
+  std::vector<int32_t> rec_seq, rec_width, rec_level;
+  std::vector<double> rec_bytes;
+  std::vector<uint64_t> rec_out;       // arena offset of each recorded op's result
+};
+
+// Plans `cones` (each the walk of one lightcone's schedule) onto one arena
+// whose first `input_elems` elements hold the inputs.
+HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems);
+
+}  // namespace qtng
