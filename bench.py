@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""QAOA MaxCut energy on B200: lightcones/s for 3-regular N=30 p=4 (BASELINE.json).
+
+One "step" = one full energy evaluation: all 45 edge lightcones of
+random_regular(30, 3, 104478) at the acceptance-scale angles
+(proj/tests/acceptance.cpp:70-71), contracted by bucket elimination.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+value : device-resident throughput -- the plan (schedules, descriptors) and the
+        gate table are in HBM; K executions of the level-batched program timed
+        with CUDA events on the library's stream, L2 flushed between steps
+        (the 512 MiB flush is outside the timed region), max over ranks.
+e2e   : the public API end to end -- energy_expectation(graph, angles) with host
+        inputs: host schedule construction, H2D of descriptors + gate table,
+        kernels, D2H of the per-edge terms (+ the NCCL reduce for N>1),
+        wall-clock, max over ranks.
+Multi-GPU: edges LPT-sharded by predicted bytes, one NCCL reduce of the terms
+(total work fixed as N grows: "strong" scaling).
+--impl reference: the reference's own energy_expectation (oracle/_ref, built
+from /root/reference unmodified), matmul backend, jobs = all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "C2": dict(n=30, d=3, seed=104478, gammas=[0.30, 0.25, 0.20, 0.15],
+               betas=[0.35, 0.30, 0.25, 0.20],
+               workload="QAOA MaxCut energy, random 3-regular N=30 p=4, seed 104478, 45 lightcones"),
+    "C4": dict(n=100, d=3, seed=1, gammas=[0.30, 0.25, 0.20], betas=[0.35, 0.30, 0.25],
+               workload="QAOA MaxCut energy, random 3-regular N=100 p=3, seed 1, 150 lightcones"),
+}
+METRIC = "QAOA MaxCut energy wall-time & lightcones/s (3-reg N=30 p=4) at 1/2/4/8 B200"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def golden_energy(name):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "energies.json")) as f:
+            return json.load(f)["configs"][name]["energy_naive"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np  # noqa: F401
+    import oracle as O
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libqtnsim_ref.so missing (build needs /root/reference)"}))
+        return 0
+    jobs = cpu_threads()
+    edges = O.ref_random_regular(cfg["n"], cfg["d"], cfg["seed"])
+    m = len(edges)
+    # One warm-up to size the sample: full energies when K of them fit in
+    # ~150 s, otherwise a rotating subset of edges per step (same metric).
+    t0 = time.perf_counter()
+    e_full, _, _, _ = O.ref_energy(cfg["n"], edges, cfg["gammas"], cfg["betas"], "matmul",
+                                   jobs=jobs)
+    t_full = time.perf_counter() - t0
+    per_step = m
+    if t_full * args.steps > 150.0:
+        per_step = max(jobs, int(m * 150.0 / (t_full * args.steps)))
+        per_step = min(per_step, m)
+    times, done = [], 0
+    for step in range(max(0, args.warmup - 1) + args.steps):
+        t0 = time.perf_counter()
+        if per_step == m:
+            O.ref_energy(cfg["n"], edges, cfg["gammas"], cfg["betas"], "matmul", jobs=jobs)
+        else:
+            sel = [(step * per_step + i) % m for i in range(per_step)]
+            O.ref_edge_terms(cfg["n"], edges, cfg["gammas"], cfg["betas"], "matmul", jobs=jobs,
+                             select=sel)
+        dt = time.perf_counter() - t0
+        if step >= max(0, args.warmup - 1):
+            times.append(dt)
+            done += per_step
+    total = sum(times)
+    value = done / total
+    sample = (f"{'full energy' if per_step == m else f'{per_step} of {m} lightcones'} per step, "
+              f"matmul backend, jobs={jobs}, OPENBLAS_NUM_THREADS=1")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "lightcones/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded random 3-regular graph)",
+        "config": {"workload": cfg["workload"], "backend": "matmul", "jobs": jobs},
+        "energy": e_full,
+        "cpu_baseline": {"value": value, "unit": "lightcones/s", "cores": jobs, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "lightcones/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(out))
+    return 0
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_06045_b200 as q
+    from paper_2204_06045_b200 import dist as qd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = q.Context(local)
+    g = q.random_regular(cfg["n"], cfg["d"], cfg["seed"])
+    a = q.Angles(cfg["gammas"], cfg["betas"])
+    p = a.depth()
+    costs = q.edge_costs(g, p)
+    shards = qd.lpt_shard(costs, world)
+    mine = shards[rank]
+    plan = q.Plan(g, p, edges=mine, ctx=ctx)
+    info = plan.info()
+
+    def energy_step_device():
+        return plan.execute(a)
+
+    # warm-up (also the parity check)
+    for _ in range(max(1, args.warmup)):
+        terms = energy_step_device()
+        plan.run_device(1)
+    full = qd.scatter_terms(g.m, mine, terms)
+    if world > 1:
+        full = qd.reduce_terms(full, dev)
+    energy = qd.energy_from_terms(g.m, full) if rank == 0 else None
+    level_ms = plan.level_ms()
+    lvl_kernel_ms = float(np.sum(level_ms))
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    clocks = ClockSampler(local)
+    # ---- value: device-resident, L2 flushed between steps
+    barrier()
+    with clocks:
+        total_ms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            total_ms += plan.run_device(1)
+        barrier()
+        # ---- e2e: public API with host inputs
+        for _ in range(max(1, args.warmup // 2)):
+            q.energy_expectation(g, a, q.GpuBackend(ctx), edges=mine)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = q.energy_expectation(g, a, q.GpuBackend(ctx), edges=mine)
+            if world > 1:
+                qd.reduce_terms(qd.scatter_terms(g.m, mine, res.terms), dev)
+        barrier()
+        e2e_s = time.perf_counter() - t0
+    total_ms = max_over_ranks(total_ms)
+    e2e_s = max_over_ranks(e2e_s)
+    lvl_kernel_ms = max_over_ranks(lvl_kernel_ms)
+
+    # largest-bucket level in isolation (C3-class microbench on real buckets)
+    big_level, big_bytes, big_ms = plan.time_level(-1, 20)
+
+    if rank != 0:
+        return 0
+    peak, peak_kind = load_peaks()
+    ms_per_step = total_ms / args.steps
+    value = g.m * args.steps / (total_ms / 1e3)
+    achieved = info.alg_bytes / (lvl_kernel_ms / 1e3) / 1e9 if world == 1 else None
+    gold = golden_energy(args.config)
+    out = {
+        "metric": METRIC, "value": value, "unit": "lightcones/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded random 3-regular graph, acceptance-scale angles)",
+        "config": {"workload": cfg["workload"], "parallelism": f"lightcone-sharded x{world}",
+                   "l2": "512 MiB flush between timed steps (outside the timed region)",
+                   "buckets": int(info.n_buckets), "levels": int(info.n_levels),
+                   "max_width": int(info.max_width)},
+        "energy": energy, "energy_golden_naive": gold,
+        "parity_bit_exact": (energy == gold) if gold is not None else None,
+        "e2e": {"value": g.m * args.steps / e2e_s, "unit": "lightcones/s",
+                "h2d_bytes_per_step": int(info.desc_bytes + 16 * (2 + 4 * p) * 4),
+                "d2h_bytes_per_step": int(16 * len(mine)),
+                "ms_per_step": 1e3 * e2e_s / args.steps,
+                "includes": "host schedule build (all edges, host threads) + H2D + kernels + D2H"},
+        "roofline": {"bound": "hbm", "kernel": "level_kernel (all levels)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "peak_source": peak_kind, "traffic": None,
+                     "alg_bytes_per_step": info.alg_bytes,
+                     "level_kernel_ms_per_step": lvl_kernel_ms},
+        "roofline_largest_level": {"level": big_level, "alg_bytes": big_bytes, "ms": big_ms,
+                                   "achieved": big_bytes / (big_ms / 1e3) / 1e9,
+                                   "frac": big_bytes / (big_ms / 1e3) / 1e9 / peak},
+        "clocks": clocks.summary(),
+        "gpu_launches": int(args.steps * info.kernels_per_run * 2),
+        "arena_bytes": int(info.arena_bytes),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(cfg):
+    """The reference's own energy_expectation on this host's cores: one full C2
+    energy (matmul backend, jobs = all threads), run in a subprocess so that
+    OPENBLAS_NUM_THREADS=1 applies."""
+    code = (
+        "import os,sys,json,time;sys.path.insert(0,%r);import oracle as O\n"
+        "c=json.loads(%r);e=O.ref_random_regular(c['n'],c['d'],c['seed'])\n"
+        "j=int(sys.argv[1]);en,w,_,_=O.ref_energy(c['n'],e,c['gammas'],c['betas'],'matmul',jobs=j)\n"
+        "print(json.dumps({'energy':en,'wall':w,'m':len(e)}))\n"
+    ) % (os.path.join(ROOT, "oracle"), json.dumps(cfg))
+    jobs = cpu_threads()
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1")
+    try:
+        r = subprocess.run([sys.executable, "-c", code, str(jobs)], capture_output=True, text=True,
+                           env=env, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        return {"value": d["m"] / d["wall"], "unit": "lightcones/s", "cores": jobs,
+                "kind": "reference", "energy": d["energy"], "wall_s": d["wall"],
+                "sample": "one full energy (all lightcones), matmul backend, "
+                          f"jobs={jobs}, OPENBLAS_NUM_THREADS=1"}
+    except Exception as ex:  # reported, not fatal
+        return {"value": None, "unit": "lightcones/s", "cores": jobs, "kind": "reference",
+                "sample": f"failed: {ex!r}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

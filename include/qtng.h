@@ -113,6 +113,14 @@ qtng_status qtng_simulate_widths(int n, int m, const int* edges, int p, int edge
 qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged,
                             double* bytes_out);
 
+/* Host-only pre-flight of energy_expectation: builds every edge's schedule and
+ * runs the data-free contract_network walk (liveness / result-width cap /
+ * routing checks, engine.cpp:160-169,246-304) and reports the first refusal
+ * in edge order exactly as qtng_energy (and the reference) would raise it:
+ * QTNG_ERR_SCHEDULE with "edge (u, v): <reason>".  No device is touched. */
+qtng_status qtng_validate_energy(int n, int m, const int* edges, int p, int merged,
+                                 int max_result_width);
+
 /* ---------------------------------------------------------------- device side */
 
 /* ContractionBackend::contract (proj/include/qtnsim/engine.hpp:30;

@@ -26,7 +26,7 @@ __all__ = [
     "CudaError", "Graph", "Edge", "Angles", "Tensor", "Bucket", "ContractionSchedule",
     "TimingRecord", "ContractionReport", "EnergyResult", "EngineConfig", "Context",
     "GpuBackend", "Plan", "make_graph", "random_regular", "edge_schedule", "simulate_widths",
-    "edge_costs", "contract_bucket", "contract_network", "energy_expectation",
+    "edge_costs", "validate_energy", "contract_bucket", "contract_network", "energy_expectation",
     "default_context", "version",
 ]
 
@@ -374,6 +374,14 @@ def edge_costs(g: Graph, p: int, merged: bool = False) -> np.ndarray:
     out = np.zeros(max(1, g.m), dtype=np.float64)
     _check(lib.qtng_edge_costs(g.n, g.m, g.flat(), p, int(merged), out))
     return out[: g.m]
+
+
+def validate_energy(g: Graph, p: int, merged: bool = False,
+                    cfg: Optional[EngineConfig] = None) -> None:
+    """Host-only pre-flight of energy_expectation: raises the ScheduleError
+    ("edge (u, v): contraction refused: ...") the reference would raise."""
+    cfg = cfg or EngineConfig()
+    _check(lib.qtng_validate_energy(g.n, g.m, g.flat(), p, int(merged), cfg.max_result_width))
 
 
 def contract_network(schedule: ContractionSchedule, backend: Optional[GpuBackend] = None,

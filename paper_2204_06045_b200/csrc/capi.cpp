@@ -362,6 +362,19 @@ qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged, d
   });
 }
 
+qtng_status qtng_validate_energy(int n, int m, const int* edges, int p, int merged,
+                                 int max_result_width) {
+  return guarded([&] {
+    if (p < 1) throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+    const Graph g = graph_from(n, m, edges);
+    const ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, selection(m, m, nullptr));
+    for (size_t i = 0; i < cs.walks.size(); ++i)
+      if (cs.walks[i].fail_code)
+        throw Error(kSchedule, "edge (" + std::to_string(cs.edges[i].u) + ", " +
+                                   std::to_string(cs.edges[i].v) + "): " + cs.walks[i].fail_msg);
+  });
+}
+
 // ---------------------------------------------------------------- one-shot device calls
 
 namespace {
