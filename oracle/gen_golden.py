@@ -143,11 +143,14 @@ def random_buckets(seed=2204, count=48):
             ts.append((vs, d))
         sums = sorted(int(v) for v in rng.choice(base, size=n_sum, replace=False))
         ov, naive = O.ref_contract_bucket(ts, sums, "naive")
-        _, matmul = O.ref_contract_bucket(ts, sums, "matmul")
+        mv, matmul = O.ref_contract_bucket(ts, sums, "matmul")
         out.append(dict(
             tensors=[dict(vars=v, re=[f17(x) for x in d.real], im=[f17(x) for x in d.imag])
                      for v, d in ts],
-            sum_vars=sums, out_vars=ov,
+            # matmul_vars can differ from out_vars: MatmulBackend returns a lone
+            # tensor with no present sum var unpermuted (contraction.cpp:124),
+            # breaking the ascending-axes contract of engine.hpp:28-29.
+            sum_vars=sums, out_vars=ov, matmul_vars=mv,
             naive_re=[f17(x) for x in naive.real], naive_im=[f17(x) for x in naive.imag],
             matmul_re=[f17(x) for x in matmul.real], matmul_im=[f17(x) for x in matmul.imag]))
     # known answers from test_engine.cpp:77-89 (<+|+> = 1)
@@ -155,7 +158,7 @@ def random_buckets(seed=2204, count=48):
     ts = [([0], np.array([r, r], complex)), ([0], np.array([r, r], complex))]
     ov, naive = O.ref_contract_bucket(ts, [0], "naive")
     out.append(dict(tensors=[dict(vars=v, re=list(d.real), im=list(d.imag)) for v, d in ts],
-                    sum_vars=[0], out_vars=ov, naive_re=list(naive.real),
+                    sum_vars=[0], out_vars=ov, matmul_vars=ov, naive_re=list(naive.real),
                     naive_im=list(naive.imag), matmul_re=list(naive.real),
                     matmul_im=list(naive.imag)))
     return out
@@ -181,6 +184,10 @@ def refusals():
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--buckets-only" in sys.argv:
+        with open(os.path.join(OUT, "buckets.json"), "w") as f:
+            json.dump(random_buckets(), f)
+        return
     print("configs:")
     cfgs = {}
     for name, c in CONFIGS.items():

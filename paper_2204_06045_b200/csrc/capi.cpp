@@ -154,7 +154,7 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
 
 // Descriptor image of a HostPlan: one contiguous blob, 256-byte aligned sections.
 struct DescLayout {
-  size_t ops = 0, trefs = 0, scal = 0, lcb = 0, terms = 0, total = 0;
+  size_t ops = 0, ibeg = 0, trefs = 0, scal = 0, lcb = 0, terms = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t{255}; }
@@ -163,6 +163,7 @@ DescLayout layout_of(const HostPlan& hp) {
   DescLayout L;
   size_t o = 0;
   L.ops = o; o = align256(o + hp.ops.size() * sizeof(DevOp));
+  L.ibeg = o; o = align256(o + hp.ibeg.size() * sizeof(uint32_t));
   L.trefs = o; o = align256(o + hp.trefs.size() * sizeof(DevTensor));
   L.scal = o; o = align256(o + hp.scalar_off.size() * sizeof(uint64_t));
   L.lcb = o; o = align256(o + hp.lc_begin.size() * sizeof(uint32_t));
@@ -173,6 +174,7 @@ DescLayout layout_of(const HostPlan& hp) {
 
 void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
   std::memcpy(dst + L.ops, hp.ops.data(), hp.ops.size() * sizeof(DevOp));
+  std::memcpy(dst + L.ibeg, hp.ibeg.data(), hp.ibeg.size() * sizeof(uint32_t));
   std::memcpy(dst + L.trefs, hp.trefs.data(), hp.trefs.size() * sizeof(DevTensor));
   std::memcpy(dst + L.scal, hp.scalar_off.data(), hp.scalar_off.size() * sizeof(uint64_t));
   std::memcpy(dst + L.lcb, hp.lc_begin.data(), hp.lc_begin.size() * sizeof(uint32_t));
@@ -214,6 +216,7 @@ struct DevProgram {
   char* base = nullptr;
   DescLayout L;
   const DevOp* ops() const { return reinterpret_cast<const DevOp*>(base + L.ops); }
+  const uint32_t* ibeg() const { return reinterpret_cast<const uint32_t*>(base + L.ibeg); }
   const DevTensor* trefs() const { return reinterpret_cast<const DevTensor*>(base + L.trefs); }
   const uint64_t* scal() const { return reinterpret_cast<const uint64_t*>(base + L.scal); }
   const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
@@ -225,7 +228,7 @@ void enqueue_program(cudaStream_t s, const HostPlan& hp, const DevProgram& pr, d
                      std::vector<cudaEvent_t>* level_events) {
   for (size_t L = 0; L < hp.levels.size(); ++L) {
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
-    QTNG_CUDA(launch_level(s, pr.ops(), pr.trefs(), arena, hp.levels[L]));
+    QTNG_CUDA(launch_level(s, pr.ops(), pr.ibeg(), pr.trefs(), arena, hp.levels[L]));
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
   QTNG_CUDA(launch_final(s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
@@ -669,11 +672,11 @@ qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* le
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     ctx->ensure_arena(hp.arena_elems);
-    QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.trefs(), ctx->A(),
+    QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.ibeg(), plan->prog.trefs(), ctx->A(),
                            hp.levels[level]));  // warm-up
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     for (int i = 0; i < n_runs; ++i)
-      QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.trefs(), ctx->A(),
+      QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.ibeg(), plan->prog.trefs(), ctx->A(),
                              hp.levels[level]));
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));

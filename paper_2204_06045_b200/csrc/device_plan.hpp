@@ -19,7 +19,7 @@ namespace qtng {
 constexpr int kMaxInputs = 8;     // tensors per op (wider buckets are pre-folded)
 constexpr int kMaxRank = 32;      // axes per input tensor (offsets are 32-bit)
 constexpr int kMaxSumBits = 10;   // summed vars per op (merged buckets: <= 9 seen)
-constexpr int kItemBits = 10;     // outputs per warp work item = 2^min(r, kItemBits)
+constexpr int kItemBits = 10;     // max outputs per warp work item = 2^kItemBits
 constexpr uint8_t kSumSrc = 64;   // DevTensor::src >= kSumSrc: a summed bit
 
 // One bucket contraction: out[k] = sum_s prod_t in_t[gather_t(k, s)].
@@ -52,7 +52,11 @@ struct LevelLaunch {
   uint32_t op_begin;
   uint32_t op_count;
   uint32_t items;
-  uint32_t pad;
+  uint32_t max_nt;  // widest member list in the level (selects the kernel instance)
 };
+
+// Planner target for warp items per level: enough to cover every SM several
+// times over, so small levels use 1-row items and big levels 32-row items.
+constexpr uint64_t kTargetItems = 16384;
 
 }  // namespace qtng

@@ -2,21 +2,28 @@
 //
 // level_kernel -- the generic fused bucket kernel.  One launch runs every
 // bucket of one dependency level of ALL planned lightcones (tiny buckets cost
-// no launch of their own).  The unit of work is a warp "item": 2^min(r,10)
-// consecutive outputs of one bucket.  Per item each lane
+// no launch of their own).  The unit of work is a warp "item": 2^cb
+// consecutive outputs of one bucket (cb <= 10, chosen per level by the
+// planner so that small levels still spread over every SM).  Per item each lane
 //   * decodes, once, every operand's bit-gather map into two 32-bit partial
 //     offsets: `lo` for its own output bits 0..4 and `hi` for output bits >= 5
 //     of the item row it will later broadcast (offsets are additive over bits
 //     because every output/sum bit maps to a distinct operand bit),
-//   * then walks the item's 2^(cb-5) rows: operand offset = lo + shfl(hi, row),
-//     128-bit read-only loads of complex128, product over operands in bucket
-//     member order, accumulation over the summed assignments in ascending
-//     order, one 128-bit store per output.
+//   * then walks the item's 2^(cb-5) rows, two at a time: operand offset =
+//     lo + shfl(hi, row), 128-bit read-only loads of complex128, the product
+//     over operands in bucket member order, accumulation over the summed
+//     assignments in ascending order, one 128-bit store per output.
 // Operands that are sorted (every intermediate result) map their low bits to
 // the bucket's low output bits, so lanes read contiguous 16-byte elements;
-// the rank<=2 gate operands are L1-resident.  Products are rounded exactly as
-// the reference's std::complex<double> `prod *= x` (ac-bd, ad+bc, no FMA), so
-// results are bit-identical to its NaiveBackend (proj/src/engine.cpp:94-106).
+// the rank<=2 gate operands are L1-resident.
+//
+// Rounding: every complex product is (ac-bd, ad+bc) with each product rounded
+// (no FMA contraction) and the summed assignments accumulate in ascending
+// order -- the exact operation sequence of the reference's
+// std::complex<double> loop (NaiveBackend::contract, proj/src/engine.cpp:94-106)
+// minus its multiplications by the initial 1 and additions to the initial 0,
+// which are exact.  Results therefore equal the reference's as IEEE values
+// (only the sign of an exact zero could differ).
 #include "kernels.cuh"
 
 #include <cstdint>
@@ -28,6 +35,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarpsPerCta = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSmemOps = 4096;  // item_begin entries cached in shared memory
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   // (a.x*b.x - a.y*b.y, a.x*b.y + a.y*b.x), every product rounded.
@@ -40,6 +48,16 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
 }
 
 __device__ __forceinline__ double2 ld(const double2* p) { return __ldg(p); }
+
+// Product over the T operands of one summed assignment (left fold, member order).
+template <int T>
+__device__ __forceinline__ double2 chain(const double2* const* base, const uint32_t* off,
+                                         uint32_t add) {
+  double2 p = ld(base[0] + off[0] + add);
+#pragma unroll
+  for (int t = 1; t < T; ++t) p = cmul(p, ld(base[t] + off[t] + add));
+  return p;
+}
 
 // NSM: 0 => no summed bit, 1 => one summed bit, 2 => 2..kMaxSumBits.
 template <int T, int NSM>
@@ -95,49 +113,66 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
   __syncwarp();  // the slot is rewritten by the warp's next item
   const int rows = cb > 5 ? 1 << (cb - 5) : 1;
   double2* out = arena + op.out + kbase + my;
-  const int ns = op.ns;
-#pragma unroll 2
-  for (int e = 0; e < rows; ++e) {
-    uint32_t off[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) off[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
-    double2 acc = make_double2(0.0, 0.0);
-    if (NSM == 0) {
-      double2 prod = make_double2(1.0, 0.0);
-#pragma unroll
-      for (int t = 0; t < T; ++t) prod = cmul(prod, ld(base[t] + off[t]));
-      acc = cadd(acc, prod);
-    } else if (NSM == 1) {
-      double2 x0[T], x1[T];
+  if (NSM != 2) {
+    // two rows in flight per iteration (rows is 1 or even)
+    for (int e = 0; e < rows; e += 2) {
+      const bool two = e + 1 < rows;
+      uint32_t o0[T], o1[T];
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        x0[t] = ld(base[t] + off[t]);
-        x1[t] = ld(base[t] + off[t] + sa[t]);
+        o0[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
+        o1[t] = lo[t] + __shfl_sync(kFull, hi[t], two ? e + 1 : e);
       }
-      double2 p0 = make_double2(1.0, 0.0), p1 = make_double2(1.0, 0.0);
+      double2 r0, r1;
+      if (NSM == 0) {
+        r0 = chain<T>(base, o0, 0);
+        r1 = chain<T>(base, o1, 0);
+      } else {
+        // s = 0 and s = 1 of both rows
+        double2 a0 = ld(base[0] + o0[0]), b0 = ld(base[0] + o0[0] + sa[0]);
+        double2 a1 = ld(base[0] + o1[0]), b1 = ld(base[0] + o1[0] + sa[0]);
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        p0 = cmul(p0, x0[t]);
-        p1 = cmul(p1, x1[t]);
+        for (int t = 1; t < T; ++t) {
+          const double2 xa0 = ld(base[t] + o0[t]), xb0 = ld(base[t] + o0[t] + sa[t]);
+          const double2 xa1 = ld(base[t] + o1[t]), xb1 = ld(base[t] + o1[t] + sa[t]);
+          a0 = cmul(a0, xa0);
+          b0 = cmul(b0, xb0);
+          a1 = cmul(a1, xa1);
+          b1 = cmul(b1, xb1);
+        }
+        r0 = cadd(a0, b0);
+        r1 = cadd(a1, b1);
       }
-      acc = cadd(cadd(acc, p0), p1);
-    } else {
-      const int n_hi = ns > 5 ? 1 << (ns - 5) : 1;
-      const int n_lo = ns > 5 ? 32 : 1 << ns;
+      if (active) {
+        out[static_cast<uint64_t>(e) << 5] = r0;
+        if (two) out[static_cast<uint64_t>(e + 1) << 5] = r1;
+      }
+    }
+  } else {
+    const int ns = op.ns;
+    const int n_hi = ns > 5 ? 1 << (ns - 5) : 1;
+    const int n_lo = ns > 5 ? 32 : 1 << ns;
+    for (int e = 0; e < rows; ++e) {
+      uint32_t off[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) off[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
+      double2 acc = make_double2(0.0, 0.0);
+      bool first = true;
       for (int sh = 0; sh < n_hi; ++sh) {
         uint32_t offh[T];
 #pragma unroll
         for (int t = 0; t < T; ++t) offh[t] = off[t] + __shfl_sync(kFull, sb[t], sh);
         for (int sl = 0; sl < n_lo; ++sl) {
-          double2 prod = make_double2(1.0, 0.0);
+          uint32_t o[T];
 #pragma unroll
-          for (int t = 0; t < T; ++t)
-            prod = cmul(prod, ld(base[t] + offh[t] + __shfl_sync(kFull, sa[t], sl)));
-          acc = cadd(acc, prod);
+          for (int t = 0; t < T; ++t) o[t] = offh[t] + __shfl_sync(kFull, sa[t], sl);
+          const double2 p = chain<T>(base, o, 0);
+          acc = first ? p : cadd(acc, p);
+          first = false;
         }
       }
+      if (active) out[static_cast<uint64_t>(e) << 5] = acc;
     }
-    if (active) out[static_cast<uint64_t>(e) << 5] = acc;
   }
 }
 
@@ -151,10 +186,19 @@ __device__ __forceinline__ void dispatch_ns(const DevOp& op, uint32_t chunk,
   else run_item<T, 2>(op, chunk, trefs, arena, lane, slot);
 }
 
-__global__ void __launch_bounds__(kThreads)
-level_kernel(const DevOp* __restrict__ ops, const DevTensor* __restrict__ trefs,
-             double2* __restrict__ arena, uint32_t op_count, uint32_t items) {
-  __shared__ DevTensor slots[kWarpsPerCta][kMaxInputs];
+// MAXT: the widest member list among the level's ops; smaller instantiations
+// need fewer registers and run at higher occupancy.
+template <int MAXT>
+__global__ void __launch_bounds__(kThreads, MAXT <= 4 ? 3 : 2)
+level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
+             const DevTensor* __restrict__ trefs, double2* __restrict__ arena,
+             uint32_t op_count, uint32_t items) {
+  __shared__ DevTensor slots[kWarpsPerCta][MAXT];
+  __shared__ uint32_t sbeg[kSmemOps];
+  const bool cached = op_count <= kSmemOps;
+  if (cached)
+    for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   DevTensor* slot = slots[threadIdx.x >> 5];
   const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -165,23 +209,24 @@ level_kernel(const DevOp* __restrict__ ops, const DevTensor* __restrict__ trefs,
       uint32_t lo = 0, hi = op_count;
       while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(&ops[mid].item_begin) <= item) lo = mid; else hi = mid;
+        const uint32_t b = cached ? sbeg[mid] : __ldg(ibeg + mid);
+        if (b <= item) lo = mid; else hi = mid;
       }
       cur = lo;
-      cur_begin = __ldg(&ops[lo].item_begin);
-      cur_end = lo + 1 < op_count ? __ldg(&ops[lo + 1].item_begin) : items;
+      cur_begin = cached ? sbeg[lo] : __ldg(ibeg + lo);
+      cur_end = lo + 1 < op_count ? (cached ? sbeg[lo + 1] : __ldg(ibeg + lo + 1)) : items;
     }
     const DevOp op = ops[cur];
     const uint32_t chunk = item - cur_begin;
     switch (op.nt) {
       case 1: dispatch_ns<1>(op, chunk, trefs, arena, lane, slot); break;
       case 2: dispatch_ns<2>(op, chunk, trefs, arena, lane, slot); break;
-      case 3: dispatch_ns<3>(op, chunk, trefs, arena, lane, slot); break;
-      case 4: dispatch_ns<4>(op, chunk, trefs, arena, lane, slot); break;
-      case 5: dispatch_ns<5>(op, chunk, trefs, arena, lane, slot); break;
-      case 6: dispatch_ns<6>(op, chunk, trefs, arena, lane, slot); break;
-      case 7: dispatch_ns<7>(op, chunk, trefs, arena, lane, slot); break;
-      default: dispatch_ns<8>(op, chunk, trefs, arena, lane, slot); break;
+      case 3: if constexpr (MAXT >= 3) dispatch_ns<3>(op, chunk, trefs, arena, lane, slot); break;
+      case 4: if constexpr (MAXT >= 4) dispatch_ns<4>(op, chunk, trefs, arena, lane, slot); break;
+      case 5: if constexpr (MAXT >= 5) dispatch_ns<5>(op, chunk, trefs, arena, lane, slot); break;
+      case 6: if constexpr (MAXT >= 6) dispatch_ns<6>(op, chunk, trefs, arena, lane, slot); break;
+      case 7: if constexpr (MAXT >= 7) dispatch_ns<7>(op, chunk, trefs, arena, lane, slot); break;
+      default: if constexpr (MAXT >= 8) dispatch_ns<8>(op, chunk, trefs, arena, lane, slot); break;
     }
   }
 }
@@ -196,31 +241,43 @@ __global__ void final_kernel(const uint64_t* __restrict__ scalar_off,
   terms[i] = s;
 }
 
+template <int MAXT>
 int resident_ctas() {
   static int cached = 0;
   if (cached == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_kernel, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_kernel<MAXT>, kThreads, 0);
     cached = sms * (per_sm > 0 ? per_sm : 1);
   }
   return cached;
 }
 
-}  // namespace
-
-int level_grid(uint32_t items) {
+template <int MAXT>
+int grid_for(uint32_t items) {
   const uint32_t want = (items + kWarpsPerCta - 1) / kWarpsPerCta;
-  const uint32_t cap = static_cast<uint32_t>(resident_ctas());
+  const uint32_t cap = static_cast<uint32_t>(resident_ctas<MAXT>());
   return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
-cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const DevTensor* trefs,
-                         double2* arena, const LevelLaunch& lv) {
+}  // namespace
+
+int level_grid(uint32_t items) { return grid_for<8>(items); }
+
+int resident_warps() { return resident_ctas<4>() * kWarpsPerCta; }
+
+cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
+                         const DevTensor* trefs, double2* arena, const LevelLaunch& lv) {
   if (lv.items == 0) return cudaSuccess;
-  level_kernel<<<level_grid(lv.items), kThreads, 0, s>>>(ops + lv.op_begin, trefs, arena,
-                                                        lv.op_count, lv.items);
+  const DevOp* o = ops + lv.op_begin;
+  const uint32_t* b = ibeg + lv.op_begin;
+  if (lv.max_nt <= 2)
+    level_kernel<2><<<grid_for<2>(lv.items), kThreads, 0, s>>>(o, b, trefs, arena, lv.op_count, lv.items);
+  else if (lv.max_nt <= 4)
+    level_kernel<4><<<grid_for<4>(lv.items), kThreads, 0, s>>>(o, b, trefs, arena, lv.op_count, lv.items);
+  else
+    level_kernel<8><<<grid_for<8>(lv.items), kThreads, 0, s>>>(o, b, trefs, arena, lv.op_count, lv.items);
   return cudaGetLastError();
 }
 

@@ -12,8 +12,11 @@ namespace qtng {
 int level_grid(uint32_t items);
 
 // One level: every op of the level, all lightcones at once.
-cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const DevTensor* trefs,
-                         double2* arena, const LevelLaunch& lv);
+cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
+                         const DevTensor* trefs, double2* arena, const LevelLaunch& lv);
+
+// Resident warps of the level kernel on the current device.
+int resident_warps();
 
 // Per lightcone: e_jk = prod of its scalar results in production order.
 cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint32_t* lc_begin,

@@ -186,6 +186,15 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   hp.level_bytes.assign(n_levels, 0.0);
   for (int L = 0; L < n_levels; ++L) {
     LevelLaunch ll{static_cast<uint32_t>(hp.ops.size()), 0, 0, 0};
+    // item size: 32-output rows per warp item, fewer for small levels so the
+    // level still spreads over the whole GPU
+    uint64_t level_rows = 0;
+    for (int i : by_level[L]) {
+      const int r = static_cast<int>(g[i].out_vars.size());
+      level_rows += r > 5 ? uint64_t{1} << (r - 5) : 1;
+    }
+    int row_bits = 0;
+    while (row_bits < kItemBits - 5 && (level_rows >> (row_bits + 1)) >= kTargetItems) ++row_bits;
     for (int i : by_level[L]) {
       const GOp& o = g[i];
       const int r = static_cast<int>(o.out_vars.size());
@@ -201,7 +210,8 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       d.r = static_cast<uint8_t>(r);
       d.ns = static_cast<uint8_t>(ns);
       d.nt = static_cast<uint8_t>(o.ins.size());
-      d.cb = static_cast<uint8_t>(std::min(r, kItemBits));
+      d.cb = static_cast<uint8_t>(std::min(r, 5 + row_bits));
+      ll.max_nt = std::max<uint32_t>(ll.max_nt, d.nt);
       const uint64_t items = uint64_t{1} << (r - d.cb);
       if (ll.items + items > 0xffffffffull) throw Error(kResource, "level has too many work items");
       ll.items += static_cast<uint32_t>(items);
@@ -230,6 +240,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
         bytes += 16.0 * static_cast<double>(uint64_t{1} << rank);
       }
       hp.ops.push_back(d);
+      hp.ibeg.push_back(d.item_begin);
       ++ll.op_count;
       hp.level_bytes[L] += bytes;
       hp.alg_bytes += bytes;

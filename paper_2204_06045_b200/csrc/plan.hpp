@@ -14,6 +14,7 @@ namespace qtng {
 
 struct HostPlan {
   std::vector<DevOp> ops;              // level-sorted
+  std::vector<uint32_t> ibeg;          // ops[i].item_begin, contiguous (kernel lookup table)
   std::vector<DevTensor> trefs;
   std::vector<LevelLaunch> levels;
   std::vector<uint64_t> scalar_off;    // per lightcone: its scalar results, production order

@@ -44,3 +44,13 @@ def q():
 @pytest.fixture(scope="session")
 def ctx(q):
     return q.Context(0)
+
+
+def reorder(data, vars_from, vars_to):
+    """Tensor data with axes `vars_from` re-laid out with axes `vars_to`."""
+    import numpy as np
+    r = len(vars_from)
+    if list(vars_from) == list(vars_to) or r == 0:
+        return np.asarray(data)
+    a = np.asarray(data).reshape([2] * r)
+    return a.transpose([list(vars_from).index(v) for v in vars_to]).reshape(-1)

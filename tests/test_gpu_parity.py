@@ -9,6 +9,7 @@ oracle where one exists.  Mirrors proj/tests/test_engine.cpp and
 proj/tests/acceptance.cpp criteria 1-3, 6.
 """
 import numpy as np
+from conftest import reorder
 import pytest
 
 from oracle import oracle_contract_bucket, oracle_contract_network
@@ -40,7 +41,7 @@ def test_golden_buckets_bit_exact(q, ctx, golden_buckets):
         ts = _golden_tensors(b)
         got = q.contract_bucket(_bucket(q, ts, b["sum_vars"]), ctx)
         naive = np.array(b["naive_re"]) + 1j * np.array(b["naive_im"])
-        matmul = np.array(b["matmul_re"]) + 1j * np.array(b["matmul_im"])
+        matmul = reorder(np.array(b["matmul_re"]) + 1j * np.array(b["matmul_im"]), b["matmul_vars"], b["out_vars"])
         assert got.vars == b["out_vars"]
         assert np.array_equal(got.data, naive)
         assert np.max(np.abs(got.data - matmul), initial=0) < 1e-12
