@@ -121,6 +121,17 @@ qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged,
 qtng_status qtng_validate_energy(int n, int m, const int* edges, int p, int merged,
                                  int max_result_width);
 
+/* Host-only dump of the device program for the selected edges (sel = NULL:
+ * all), for analysis and tests.  Per device op (level-sorted), 8 ints:
+ *   level, r (result rank), ns (summed bits), nt (inputs), cb (log2 outputs
+ *   per work item), recorded (0 for a pre-fold helper), width, 0
+ * then per input 34 ints: rank, initial (1 = gate/input-region tensor),
+ *   src[32] (kMaxRank axis sources; <64 output bit, >=64 summed bit 64+j).
+ * *n_ints receives the size needed; nothing is written if cap is short. */
+qtng_status qtng_plan_dump(int n, int m, const int* edges, int p, int merged,
+                           int max_result_width, int n_sel, const int* sel, int* ints,
+                           int64_t cap, int64_t* n_ints, int* n_ops);
+
 /* ---------------------------------------------------------------- device side */
 
 /* ContractionBackend::contract (proj/include/qtnsim/engine.hpp:30;

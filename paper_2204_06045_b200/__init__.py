@@ -376,6 +376,35 @@ def edge_costs(g: Graph, p: int, merged: bool = False) -> np.ndarray:
     return out[: g.m]
 
 
+def plan_dump(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfig] = None,
+              edges: Optional[Sequence[int]] = None) -> List[dict]:
+    """Host-only description of the device program (one dict per device op,
+    level-sorted): level, r, ns, nt, cb, recorded, width, inputs=[(rank,
+    initial, src list)]."""
+    cfg = cfg or EngineConfig()
+    sel = None if edges is None else np.ascontiguousarray(edges, dtype=np.int32)
+    k = g.m if sel is None else len(sel)
+    sp = None if sel is None else sel.ctypes.data_as(C.c_void_p)
+    n_ints, n_ops = C.c_int64(0), C.c_int(0)
+    probe = np.zeros(1, np.int32)
+    _check(lib.qtng_plan_dump(g.n, g.m, g.flat(), p, int(merged), cfg.max_result_width, k, sp,
+                              probe, 0, C.byref(n_ints), C.byref(n_ops)))
+    buf = np.zeros(max(1, n_ints.value), np.int32)
+    _check(lib.qtng_plan_dump(g.n, g.m, g.flat(), p, int(merged), cfg.max_result_width, k, sp,
+                              buf, len(buf), C.byref(n_ints), C.byref(n_ops)))
+    out, i = [], 0
+    for _ in range(n_ops.value):
+        lv, r, ns, nt, cb, rec, w, _z = (int(x) for x in buf[i:i + 8])
+        i += 8
+        ins = []
+        for _ in range(nt):
+            rank, init = int(buf[i]), int(buf[i + 1])
+            ins.append((rank, init, [int(x) for x in buf[i + 2:i + 2 + rank]]))
+            i += 34
+        out.append(dict(level=lv, r=r, ns=ns, nt=nt, cb=cb, recorded=rec, width=w, inputs=ins))
+    return out
+
+
 def validate_energy(g: Graph, p: int, merged: bool = False,
                     cfg: Optional[EngineConfig] = None) -> None:
     """Host-only pre-flight of energy_expectation: raises the ScheduleError

@@ -378,6 +378,39 @@ qtng_status qtng_validate_energy(int n, int m, const int* edges, int p, int merg
   });
 }
 
+qtng_status qtng_plan_dump(int n, int m, const int* edges, int p, int merged,
+                           int max_result_width, int n_sel, const int* sel, int* ints,
+                           int64_t cap, int64_t* n_ints, int* n_ops) {
+  return guarded([&] {
+    if (p < 1) throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+    const Graph g = graph_from(n, m, edges);
+    const ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, selection(m, n_sel, sel));
+    std::vector<const WalkResult*> ptrs;
+    for (const WalkResult& w : cs.walks) {
+      if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
+      ptrs.push_back(&w);
+    }
+    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems);
+    std::vector<int> out;
+    for (size_t L = 0; L < hp.levels.size(); ++L)
+      for (uint32_t k = 0; k < hp.levels[L].op_count; ++k) {
+        const uint32_t i = hp.levels[L].op_begin + k;
+        const DevOp& d = hp.ops[i];
+        out.insert(out.end(), {static_cast<int>(L), d.r, d.ns, d.nt, d.cb,
+                               hp.op_width[i] > 0 ? 1 : 0, hp.op_width[i], 0});
+        for (int t = 0; t < d.nt; ++t) {
+          const DevTensor& x = hp.trefs[d.tref + t];
+          out.push_back(x.rank);
+          out.push_back(x.off < hp.input_elems ? 1 : 0);
+          for (int a = 0; a < kMaxRank; ++a) out.push_back(a < x.rank ? x.src[a] : -1);
+        }
+      }
+    *n_ints = static_cast<int64_t>(out.size());
+    *n_ops = static_cast<int>(hp.ops.size());
+    if (static_cast<int64_t>(out.size()) <= cap) std::copy(out.begin(), out.end(), ints);
+  });
+}
+
 // ---------------------------------------------------------------- one-shot device calls
 
 namespace {

@@ -32,9 +32,14 @@ struct alignas(16) DevOp {
   uint8_t r;            // result rank
   uint8_t ns;           // summed bits
   uint8_t nt;           // inputs (1..kMaxInputs), in bucket member order
-  uint8_t cb;           // log2(outputs per work item) = min(r, kItemBits)
-  uint32_t pad;
+  uint8_t cb;           // log2(outputs per work item), <= kItemBits
+  // Register-tiling bits: output bits in [5, cb) whose 2 (or 4) combinations a
+  // lane computes together, sharing the loads of every operand that lacks
+  // them (the planner picks them from the operands' bit sets).  kNoBit = unused.
+  uint8_t rb[2];
+  uint8_t pad[2];
 };
+constexpr uint8_t kNoBit = 0xff;
 static_assert(sizeof(DevOp) == 32, "DevOp layout");
 
 // An input operand: its arena offset and, per axis (MSB first), where the

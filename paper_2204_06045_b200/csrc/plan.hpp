@@ -15,6 +15,7 @@ namespace qtng {
 struct HostPlan {
   std::vector<DevOp> ops;              // level-sorted
   std::vector<uint32_t> ibeg;          // ops[i].item_begin, contiguous (kernel lookup table)
+  std::vector<int32_t> op_width;       // bucket width per device op, 0 for pre-fold helpers
   std::vector<DevTensor> trefs;
   std::vector<LevelLaunch> levels;
   std::vector<uint64_t> scalar_off;    // per lightcone: its scalar results, production order
