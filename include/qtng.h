@@ -169,6 +169,13 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
 qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int p, int merged,
                              int max_result_width, int n_sel, const int* sel,
                              qtng_plan** out);
+/* Device-resident plan of ONE explicit schedule (format of qtng_edge_schedule),
+ * e.g. a single wide bucket for the C3 microbenchmark.  Its initial tensor
+ * data is uploaded once; qtng_plan_execute then ignores the angles and
+ * returns the schedule's scalar as terms[0..1]. */
+qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* ints,
+                                      int64_t n_ints, const double* data, int max_result_width,
+                                      qtng_plan** out);
 /* Run the plan for one angle set.  terms (host, may be NULL) receives
  * 2*n_sel doubles.  device_ms (may be NULL) = device time of the kernels
  * (CUDA events on the plan's stream). */

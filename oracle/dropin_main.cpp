@@ -30,7 +30,7 @@ int main(int argc, char** argv) {
   const Graph g = random_regular(n, 3, seed);
   qtng::GpuBackend gpu(0);
   const NaiveBackend naive;
-  const MixedBackend mixed(6, naive, gpu);  // width <= 6 on the CPU, wider on the B200
+  const MixedBackend mixed(3, naive, gpu);  // width <= 3 on the CPU, wider on the B200
   const EnergyResult r_naive = energy_expectation(g, a, naive, false);
   const EnergyResult r_gpu = energy_expectation(g, a, gpu, false);
   const EnergyResult r_gpu4 = energy_expectation(g, a, gpu, false, {}, 4);
@@ -39,7 +39,7 @@ int main(int argc, char** argv) {
   for (const TimingRecord& rec : r_mixed.report.records) {
     const bool hi = rec.backend == "b200";
     (hi ? gpu_recs : low_recs)++;
-    if (hi != (rec.width > 6)) ++bad_dispatch;
+    if (hi != (rec.width > 3)) ++bad_dispatch;
   }
   bool all_b200 = true;
   for (const TimingRecord& rec : r_gpu.report.records) all_b200 &= rec.backend == "b200";

@@ -480,14 +480,36 @@ class Plan:
         _check(lib.qtng_plan_info_get(self._h, C.byref(inf)))
         return inf
 
-    def execute(self, angles: Angles) -> np.ndarray:
+    @classmethod
+    def from_schedule(cls, schedule: ContractionSchedule, cfg: Optional[EngineConfig] = None,
+                      ctx: Optional[Context] = None) -> "Plan":
+        """Device-resident plan of one explicit schedule (e.g. a single wide
+        bucket); execute() returns its scalar as a 1-element array."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        cfg = cfg or EngineConfig()
+        self.graph, self.p, self.sel = None, 0, np.zeros(1, np.int32)
+        ints, n_ints, data = schedule.flatten()
+        h = C.c_void_p()
+        _check(lib.qtng_plan_create_schedule(self.ctx.handle, len(schedule.buckets), ints, n_ints,
+                                             np.ascontiguousarray(data), cfg.max_result_width,
+                                             C.byref(h)))
+        self._h = h
+        self.last_device_ms = 0.0
+        return self
+
+    def execute(self, angles: Optional[Angles] = None) -> np.ndarray:
         """Per-edge complex e_jk of the selected edges (selection order)."""
-        gam, bet = _angles_arrays(angles)
-        if len(gam) != self.p or len(bet) != self.p:
-            raise InvalidInputError("angles: gammas and betas must have equal length p >= 1")
+        if self.p:
+            gam, bet = _angles_arrays(angles)
+            if len(gam) != self.p or len(bet) != self.p:
+                raise InvalidInputError("angles: gammas and betas must have equal length p >= 1")
+            gp, bp = gam.ctypes.data_as(C.c_void_p), bet.ctypes.data_as(C.c_void_p)
+        else:
+            gp = bp = None
         out = np.zeros(2 * max(1, len(self.sel)), np.float64)
         ms = C.c_float(0)
-        _check(lib.qtng_plan_execute(self._h, gam, bet, out.ctypes.data_as(C.c_void_p),
+        _check(lib.qtng_plan_execute(self._h, gp, bp, out.ctypes.data_as(C.c_void_p),
                                      C.byref(ms)))
         self.last_device_ms = ms.value
         return out[: 2 * len(self.sel)].view(np.complex128).copy()

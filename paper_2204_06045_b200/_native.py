@@ -11,7 +11,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqtng.so")
+LIB_PATH = os.environ.get("QTNG_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libqtng.so")  # override: kernel tuning runs
 
 i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
@@ -69,7 +70,9 @@ def _load():
                                 C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_double), f64p]
     lib.qtng_plan_create.argtypes = [vp, C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int,
                                      C.c_int, C.c_void_p, pvp]
-    lib.qtng_plan_execute.argtypes = [vp, f64p, f64p, C.c_void_p, C.POINTER(C.c_float)]
+    lib.qtng_plan_create_schedule.argtypes = [vp, C.c_int, i32p, C.c_int64, f64p, C.c_int, pvp]
+    lib.qtng_plan_execute.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.POINTER(C.c_float)]
     lib.qtng_plan_run_device.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
     lib.qtng_plan_info_get.argtypes = [vp, C.POINTER(PlanInfo)]
     lib.qtng_plan_records.argtypes = [vp, C.POINTER(Record), C.c_int64, C.POINTER(C.c_int64)]
@@ -87,7 +90,7 @@ lib = _load()
 EXPORTED = [
     "qtng_create", "qtng_destroy", "qtng_last_error", "qtng_version", "qtng_random_regular",
     "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
-    "qtng_contract_schedule", "qtng_energy", "qtng_plan_create", "qtng_plan_execute",
+    "qtng_contract_schedule", "qtng_energy", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute",
     "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_records", "qtng_plan_level_ms",
     "qtng_plan_destroy", "qtng_plan_time_level",
 ]

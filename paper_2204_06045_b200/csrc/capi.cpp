@@ -252,6 +252,7 @@ struct qtng_plan {
   HostPlan hp;
   std::vector<Edge> edges;
   int p = 0;
+  bool explicit_sched = false;  // qtng_plan_create_schedule: input region = pin_gate as given
   DevBuf desc;
   DevProgram prog;
   PinBuf pin_gate, pin_terms;
@@ -573,17 +574,55 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
   });
 }
 
+qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* ints,
+                                      int64_t n_ints, const double* data, int max_result_width,
+                                      qtng_plan** out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error(kInvalidInput, "null argument");
+    const Schedule s = parse_schedule(n_buckets, ints, static_cast<long>(n_ints));
+    const WalkResult w = walk_schedule(s, max_result_width);
+    if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
+    if (w.ops.empty()) throw Error(kInvalidInput, "schedule has no non-empty bucket");
+    uint64_t input_elems = 0;
+    for (const SchedTensor& t : s.init) input_elems += uint64_t{1} << t.vars.size();
+    auto plan = std::make_unique<qtng_plan>();
+    plan->ctx = ctx;
+    plan->explicit_sched = true;
+    plan->edges = {Edge{-1, -1}};
+    plan->hp = build_plan({&w}, input_elems);
+    const HostPlan& hp = plan->hp;
+    const DescLayout L = layout_of(hp);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    plan->desc.ensure(L.total);
+    plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L};
+    ctx->pin_desc.ensure(L.total);
+    pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
+    QTNG_CUDA(cudaMemcpyAsync(plan->desc.p, ctx->pin_desc.p, L.total, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    plan->pin_gate.ensure(std::max<uint64_t>(input_elems, 1) * sizeof(double2));
+    std::memcpy(plan->pin_gate.p, data, input_elems * sizeof(double2));
+    plan->pin_terms.ensure(sizeof(double2));
+    plan->lev_ev.resize(hp.levels.size() + 1);
+    for (cudaEvent_t& e : plan->lev_ev) QTNG_CUDA(cudaEventCreate(&e));
+    plan->level_ms.assign(hp.levels.size(), 0.f);
+    *out = plan.release();
+  });
+}
+
 qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const double* betas,
                               double* terms, float* device_ms) {
   return guarded([&] {
     if (!plan) throw Error(kInvalidInput, "null plan");
-    validate_angles(plan->p, gammas, betas);
+    if (!plan->explicit_sched) validate_angles(plan->p, gammas, betas);
     qtng_ctx* ctx = plan->ctx;
     const HostPlan& hp = plan->hp;
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     ctx->ensure_arena(hp.arena_elems);
-    fill_gate_table(plan->p, gammas, betas, static_cast<double*>(plan->pin_gate.p));
+    if (!plan->explicit_sched)
+      fill_gate_table(plan->p, gammas, betas, static_cast<double*>(plan->pin_gate.p));
     QTNG_CUDA(cudaMemcpyAsync(ctx->A(), plan->pin_gate.p, hp.input_elems * sizeof(double2),
                               cudaMemcpyHostToDevice, ctx->stream));
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -600,7 +639,7 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     if (device_ms) *device_ms = ms;
     const double* t = static_cast<const double*>(plan->pin_terms.p);
     if (terms) std::memcpy(terms, t, nb);
-    check_terms(plan->edges, t);
+    if (!plan->explicit_sched) check_terms(plan->edges, t);
   });
 }
 

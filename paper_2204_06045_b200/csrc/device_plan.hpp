@@ -33,13 +33,12 @@ struct alignas(16) DevOp {
   uint8_t ns;           // summed bits
   uint8_t nt;           // inputs (1..kMaxInputs), in bucket member order
   uint8_t cb;           // log2(outputs per work item), <= kItemBits
-  // Register-tiling bits: output bits in [5, cb) whose 2 (or 4) combinations a
-  // lane computes together, sharing the loads of every operand that lacks
-  // them (the planner picks them from the operands' bit sets).  kNoBit = unused.
-  uint8_t rb[2];
-  uint8_t pad[2];
+  // 1 when member 0 is row-invariant inside a work item (it has no output bit
+  // in [5, cb), e.g. the gate on the summed variable): the kernel then loads
+  // it once per item instead of once per row.  Only set for ns == 1, nt >= 2.
+  uint8_t inv0;
+  uint8_t pad[3];
 };
-constexpr uint8_t kNoBit = 0xff;
 static_assert(sizeof(DevOp) == 32, "DevOp layout");
 
 // An input operand: its arena offset and, per axis (MSB first), where the

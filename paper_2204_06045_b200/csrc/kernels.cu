@@ -4,21 +4,17 @@
 // bucket of one dependency level of ALL planned lightcones (tiny buckets cost
 // no launch of their own).  The unit of work is a warp "item": 2^cb
 // consecutive outputs of one bucket (cb <= 10, chosen per level by the
-// planner so that small levels still spread over every SM).  An item is a
-// set of 32-output "rows" (lanes = output bits 0..4).  Per item each lane
-//   * decodes, once, every operand's bit-gather map into 32-bit partial
-//     offsets: `lo` for its own output bits 0..4, `hi` for output bits >= 5 of
-//     the row it will later broadcast, and d0/d1 = the operand strides of the
-//     two register-tiling bits (offsets are additive over bits because every
-//     output/summed bit maps to a distinct operand bit),
-//   * then walks the item's rows 2^NR at a time (the rows differing in the
-//     planner-chosen register bits): operand offset = lo + shfl(hi, row) +
-//     {0, d0, d1, d0+d1}; an operand that lacks a register bit is loaded once
-//     for both rows (warp-uniform branch), so outer-join buckets -- two large
-//     operands over disjoint bits -- issue ~half the loads per output.
-//     128-bit read-only loads of complex128, the product over operands in
-//     bucket member order, accumulation over the summed assignments in
-//     ascending order, one 128-bit store per output.
+// planner so that small levels still spread over every SM).  Per item each lane
+//   * decodes, once, every operand's bit-gather map into two 32-bit partial
+//     offsets: `lo` for its own output bits 0..4 and `hi` for output bits >= 5
+//     of the item row it will later broadcast (offsets are additive over bits
+//     because every output/sum bit maps to a distinct operand bit),
+//   * then walks the item's 2^(cb-5) rows, two at a time: operand offset =
+//     lo + shfl(hi, row), 128-bit read-only loads of complex128, the product
+//     over operands in bucket member order, accumulation over the summed
+//     assignments in ascending order, one 128-bit store per output.  A
+//     leading member without row bits (typically the gate on the summed
+//     variable) is loaded once per item.
 // Operands that are sorted (every intermediate result) map their low bits to
 // the bucket's low output bits, so lanes read contiguous 16-byte elements;
 // the rank<=2 gate operands are L1-resident.
@@ -57,57 +53,48 @@ __device__ __forceinline__ double2 ld(const double2* p) { return __ldg(p); }
 
 // Product over the T operands of one summed assignment (left fold, member order).
 template <int T>
-__device__ __forceinline__ double2 chain(const double2* const* base, const uint32_t* off) {
-  double2 p = ld(base[0] + off[0]);
+__device__ __forceinline__ double2 chain(const double2* const* base, const uint32_t* off,
+                                         uint32_t add) {
+  double2 p = ld(base[0] + off[0] + add);
 #pragma unroll
-  for (int t = 1; t < T; ++t) p = cmul(p, ld(base[t] + off[t]));
+  for (int t = 1; t < T; ++t) p = cmul(p, ld(base[t] + off[t] + add));
   return p;
 }
 
-// Insert a zero bit at position q of x (q < 32).
-__device__ __forceinline__ uint32_t insert_zero(uint32_t x, uint32_t q) {
-  const uint32_t low = x & ((1u << q) - 1u);
-  return ((x >> q) << (q + 1)) | low;
-}
-
-// Per-lane decode of the op's operands (see the file comment).
-template <int T, int NSM>
-struct Decoded {
-  const double2* base[T];
-  uint32_t lo[T], hi[T], sa[T], sb[T], d0[T], d1[T];
-};
-
-template <int T, int NSM>
-__device__ __forceinline__ void decode(const DevOp& op, uint64_t kbase, uint32_t my, int lane,
-                                       const DevTensor* __restrict__ trefs,
-                                       double2* __restrict__ arena, DevTensor* slot,
-                                       Decoded<T, NSM>& D) {
+// NSM: 0 => no summed bit, 1 => one summed bit, 2 => 2..kMaxSumBits.
+// K: 1 => member 0 is row-invariant (DevOp::inv0), hoisted out of the row loop.
+template <int T, int NSM, int K>
+__device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
+                                         const DevTensor* __restrict__ trefs,
+                                         double2* __restrict__ arena, int lane,
+                                         DevTensor* slot) {
+  const int cb = op.cb;
+  const uint64_t kbase = static_cast<uint64_t>(chunk) << cb;
+  const bool active = cb >= 5 || lane < (1 << cb);
+  const uint32_t my = active ? lane : 0;
   const uint64_t khi = kbase | (static_cast<uint64_t>(lane) << 5);  // lane = row for `hi`
-  const uint32_t r0 = op.rb[0], r1 = op.rb[1];
   // Stage the op's operand descriptors in this warp's shared slot; the
-  // per-axis decode then reads its source bits with broadcast LDS.
+  // per-axis decode below then reads its source bits with broadcast LDS.
   {
     const uint4* src4 = reinterpret_cast<const uint4*>(trefs + op.tref);
     uint4* dst4 = reinterpret_cast<uint4*>(slot);
     if (lane < 3 * T) dst4[lane] = __ldg(src4 + lane);
     __syncwarp();
   }
+  const double2* base[T];
+  uint32_t lo[T], hi[T], sa[T], sb[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) {
     const DevTensor& d = slot[t];
-    D.base[t] = arena + d.off;
+    base[t] = arena + d.off;
     const int rank = d.rank;
-    uint32_t l = 0, h = 0, a = 0, b = 0, x0 = 0, x1 = 0;
+    uint32_t l = 0, h = 0, a = 0, b = 0;
 #pragma unroll 1
     for (int ax = 0; ax < rank; ++ax) {
       const uint32_t src = d.src[ax];
       const uint32_t bit = 1u << (rank - 1 - ax);
       if (src < 5) {
         l |= ((my >> src) & 1u) ? bit : 0u;
-      } else if (src == r0) {
-        x0 |= bit;
-      } else if (src == r1) {
-        x1 |= bit;
       } else if (src < kSumSrc) {
         h |= ((khi >> src) & 1u) ? bit : 0u;
       } else {
@@ -121,124 +108,89 @@ __device__ __forceinline__ void decode(const DevOp& op, uint64_t kbase, uint32_t
         }
       }
     }
-    D.lo[t] = l;
-    D.hi[t] = h;
-    D.sa[t] = a;
-    D.sb[t] = b;
-    D.d0[t] = x0;
-    D.d1[t] = x1;
+    lo[t] = l;
+    hi[t] = h;
+    sa[t] = a;
+    sb[t] = b;
   }
   __syncwarp();  // the slot is rewritten by the warp's next item
-}
-
-// Loads of operand t for the (up to) four register-tile rows, deduplicated
-// when the operand lacks a register bit (d == 0, warp-uniform).
-template <int NR>
-__device__ __forceinline__ void load_tile(const double2* p, uint32_t d0, uint32_t d1,
-                                          double2 (&x)[1 << NR]) {
-  x[0] = ld(p);
-  if (NR >= 1) x[1] = d0 ? ld(p + d0) : x[0];
-  if (NR >= 2) {
-    if (d1) {
-      x[2] = ld(p + d1);
-      x[3] = d0 ? ld(p + d0 + d1) : x[2];
-    } else {
-      x[2] = x[0];
-      x[3] = x[1];
-    }
-  }
-}
-
-// NSM: 0 => no summed bit, 1 => one summed bit.  NR: log2 rows per step.
-template <int T, int NSM, int NR>
-__device__ __forceinline__ void run_rows(const DevOp& op, uint32_t chunk,
-                                         const DevTensor* __restrict__ trefs,
-                                         double2* __restrict__ arena, int lane, DevTensor* slot) {
-  const int cb = op.cb;
-  const uint64_t kbase = static_cast<uint64_t>(chunk) << cb;
-  const bool active = cb >= 5 || lane < (1 << cb);
-  const uint32_t my = active ? lane : 0;
-  Decoded<T, NSM> D;
-  decode<T, NSM>(op, kbase, my, lane, trefs, arena, slot, D);
-  // register bits relative to the row index (output bit 5 = row bit 0)
-  const bool v0 = NR >= 1 && op.rb[0] != kNoBit;
-  const bool v1 = NR >= 2 && op.rb[1] != kNoBit;
-  const uint32_t q0 = v0 ? op.rb[0] - 5u : 0u, q1 = v1 ? op.rb[1] - 5u : 0u;
   const int rows = cb > 5 ? 1 << (cb - 5) : 1;
-  const int steps = rows >> ((v0 ? 1 : 0) + (v1 ? 1 : 0));
   double2* out = arena + op.out + kbase + my;
-  constexpr int J = 1 << NR;
-  for (int it = 0; it < steps; ++it) {
-    uint32_t e = it;
-    if (v0) e = insert_zero(e, q0);
-    if (v1) e = insert_zero(e, q1);
-    const double2* p[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) p[t] = D.base[t] + D.lo[t] + __shfl_sync(kFull, D.hi[t], e);
-    double2 acc[J];
-#pragma unroll
-    for (int s = 0; s < (NSM == 1 ? 2 : 1); ++s) {
-      double2 prod[J];
+  if (NSM != 2) {
+    double2 g0 = make_double2(0.0, 0.0), g1 = g0;
+    if (K == 1) {  // member 0 has no row bit: one load per item, both summed values
+      const uint32_t o = lo[0] + __shfl_sync(kFull, hi[0], 0);
+      g0 = ld(base[0] + o);
+      g1 = ld(base[0] + o + sa[0]);
+    }
+    // two rows in flight per iteration (rows is 1 or even)
+    for (int e = 0; e < rows; e += 2) {
+      const bool two = e + 1 < rows;
+      uint32_t o0[T], o1[T];
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        double2 x[J];
-        load_tile<NR>(p[t] + (s ? D.sa[t] : 0u), D.d0[t], D.d1[t], x);
-#pragma unroll
-        for (int j = 0; j < J; ++j) prod[j] = t == 0 ? x[j] : cmul(prod[j], x[j]);
+        o0[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
+        o1[t] = lo[t] + __shfl_sync(kFull, hi[t], two ? e + 1 : e);
       }
+      double2 r0, r1;
+      if (NSM == 0) {
+        r0 = chain<T>(base, o0, 0);
+        r1 = chain<T>(base, o1, 0);
+      } else {
+        // s = 0 and s = 1 of both rows; a row-invariant member 0 (K == 1) was
+        // loaded once for the whole item
+        double2 a0, b0, a1, b1;
+        if (K == 1) {
+          a0 = a1 = g0;
+          b0 = b1 = g1;
+        } else {
+          a0 = ld(base[0] + o0[0]);
+          b0 = ld(base[0] + o0[0] + sa[0]);
+          a1 = ld(base[0] + o1[0]);
+          b1 = ld(base[0] + o1[0] + sa[0]);
+        }
 #pragma unroll
-      for (int j = 0; j < J; ++j) acc[j] = s == 0 ? prod[j] : cadd(acc[j], prod[j]);
-    }
-    if (active) {
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        if ((j & 1) && !v0) continue;
-        if ((j & 2) && !v1) continue;
-        const uint32_t row = e | ((j & 1) ? 1u << q0 : 0u) | ((j & 2) ? 1u << q1 : 0u);
-        out[static_cast<uint64_t>(row) << 5] = acc[j];
+        for (int t = 1; t < T; ++t) {
+          const double2 xa0 = ld(base[t] + o0[t]), xb0 = ld(base[t] + o0[t] + sa[t]);
+          const double2 xa1 = ld(base[t] + o1[t]), xb1 = ld(base[t] + o1[t] + sa[t]);
+          a0 = cmul(a0, xa0);
+          b0 = cmul(b0, xb0);
+          a1 = cmul(a1, xa1);
+          b1 = cmul(b1, xb1);
+        }
+        r0 = cadd(a0, b0);
+        r1 = cadd(a1, b1);
       }
-    }
-  }
-}
-
-// Two or more summed bits (merged buckets): one row at a time, the summed
-// assignments enumerated in ascending order through two shuffle tables.
-template <int T>
-__device__ __forceinline__ void run_multisum(const DevOp& op, uint32_t chunk,
-                                             const DevTensor* __restrict__ trefs,
-                                             double2* __restrict__ arena, int lane,
-                                             DevTensor* slot) {
-  const int cb = op.cb;
-  const uint64_t kbase = static_cast<uint64_t>(chunk) << cb;
-  const bool active = cb >= 5 || lane < (1 << cb);
-  const uint32_t my = active ? lane : 0;
-  Decoded<T, 2> D;
-  decode<T, 2>(op, kbase, my, lane, trefs, arena, slot, D);
-  const int rows = cb > 5 ? 1 << (cb - 5) : 1;
-  double2* out = arena + op.out + kbase + my;
-  const int ns = op.ns;
-  const int n_hi = ns > 5 ? 1 << (ns - 5) : 1;
-  const int n_lo = ns > 5 ? 32 : 1 << ns;
-  for (int e = 0; e < rows; ++e) {
-    uint32_t off[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) off[t] = D.lo[t] + __shfl_sync(kFull, D.hi[t], e);
-    double2 acc = make_double2(0.0, 0.0);
-    bool first = true;
-    for (int sh = 0; sh < n_hi; ++sh) {
-      uint32_t offh[T];
-#pragma unroll
-      for (int t = 0; t < T; ++t) offh[t] = off[t] + __shfl_sync(kFull, D.sb[t], sh);
-      for (int sl = 0; sl < n_lo; ++sl) {
-        uint32_t o[T];
-#pragma unroll
-        for (int t = 0; t < T; ++t) o[t] = offh[t] + __shfl_sync(kFull, D.sa[t], sl);
-        const double2 p = chain<T>(D.base, o);
-        acc = first ? p : cadd(acc, p);
-        first = false;
+      if (active) {
+        out[static_cast<uint64_t>(e) << 5] = r0;
+        if (two) out[static_cast<uint64_t>(e + 1) << 5] = r1;
       }
     }
-    if (active) out[static_cast<uint64_t>(e) << 5] = acc;
+  } else {
+    const int ns = op.ns;
+    const int n_hi = ns > 5 ? 1 << (ns - 5) : 1;
+    const int n_lo = ns > 5 ? 32 : 1 << ns;
+    for (int e = 0; e < rows; ++e) {
+      uint32_t off[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) off[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
+      double2 acc = make_double2(0.0, 0.0);
+      bool first = true;
+      for (int sh = 0; sh < n_hi; ++sh) {
+        uint32_t offh[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) offh[t] = off[t] + __shfl_sync(kFull, sb[t], sh);
+        for (int sl = 0; sl < n_lo; ++sl) {
+          uint32_t o[T];
+#pragma unroll
+          for (int t = 0; t < T; ++t) o[t] = offh[t] + __shfl_sync(kFull, sa[t], sl);
+          const double2 p = chain<T>(base, o, 0);
+          acc = first ? p : cadd(acc, p);
+          first = false;
+        }
+      }
+      if (active) out[static_cast<uint64_t>(e) << 5] = acc;
+    }
   }
 }
 
@@ -248,19 +200,25 @@ __device__ __forceinline__ void dispatch_ns(const DevOp& op, uint32_t chunk,
                                             double2* __restrict__ arena, int lane,
                                             DevTensor* slot) {
   if (op.ns == 1) {
-    if (T <= 4 && op.rb[1] != kNoBit) run_rows<T, 1, (T <= 4 ? 2 : 1)>(op, chunk, trefs, arena, lane, slot);
-    else run_rows<T, 1, 1>(op, chunk, trefs, arena, lane, slot);
+    if (T >= 2 && op.inv0) run_item<T, 1, 1>(op, chunk, trefs, arena, lane, slot);
+    else run_item<T, 1, 0>(op, chunk, trefs, arena, lane, slot);
   } else if (op.ns == 0) {
-    run_rows<T, 0, 1>(op, chunk, trefs, arena, lane, slot);
+    run_item<T, 0, 0>(op, chunk, trefs, arena, lane, slot);
   } else {
-    run_multisum<T>(op, chunk, trefs, arena, lane, slot);
+    run_item<T, 2, 0>(op, chunk, trefs, arena, lane, slot);
   }
 }
 
 // MAXT: the widest member list among the level's ops; smaller instantiations
 // need fewer registers and run at higher occupancy.
 template <int MAXT>
-__global__ void __launch_bounds__(kThreads, MAXT <= 2 ? 3 : 2)
+#ifndef QTNG_MINB_T2
+#define QTNG_MINB_T2 4  // CTAs/SM the register budget must allow (tuned: tools/tune.py)
+#endif
+#ifndef QTNG_MINB_T4
+#define QTNG_MINB_T4 3
+#endif
+__global__ void __launch_bounds__(kThreads, MAXT <= 2 ? QTNG_MINB_T2 : (MAXT <= 4 ? QTNG_MINB_T4 : 2))
 level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
              const DevTensor* __restrict__ trefs, double2* __restrict__ arena,
              uint32_t op_count, uint32_t items) {

@@ -93,41 +93,16 @@ struct GOp {
 
 uint64_t out_alloc_size(int r) { return round_up(uint64_t{1} << r, kAlign); }
 
-// Register tiling (kernels.cu run_rows): a lane computes the 2 or 4 rows that
-// differ in rb[0]/rb[1]; an operand lacking such a bit is loaded once for
-// them.  Cost = operand loads per output; pick the bits minimising it.
-void choose_register_bits(DevOp& d, const DevTensor* ts) {
-  d.rb[0] = d.rb[1] = kNoBit;
-  const int row_bits = d.cb > 5 ? d.cb - 5 : 0;
-  if (row_bits == 0 || d.ns > 1) return;
-  uint64_t mask[kMaxInputs] = {};
-  for (int t = 0; t < d.nt; ++t)
-    for (int ax = 0; ax < ts[t].rank; ++ax)
-      if (ts[t].src[ax] < kSumSrc) mask[t] |= uint64_t{1} << ts[t].src[ax];
-  auto cost = [&](int b0, int b1) {
-    double c = 0;
-    for (int t = 0; t < d.nt; ++t) {
-      const int k = (b0 >= 0 && ((mask[t] >> b0) & 1)) + (b1 >= 0 && ((mask[t] >> b1) & 1));
-      c += static_cast<double>(1 << k);
-    }
-    return c / static_cast<double>(1 << ((b0 >= 0) + (b1 >= 0)));
-  };
-  int best0 = 5;
-  double c1 = cost(5, -1);
-  for (int b = 6; b < 5 + row_bits; ++b)
-    if (cost(b, -1) < c1 - 1e-9) { c1 = cost(b, -1); best0 = b; }
-  d.rb[0] = static_cast<uint8_t>(best0);
-  if (d.ns == 1 && d.nt <= 4 && row_bits >= 2) {
-    int p0 = -1, p1 = -1;
-    double c2 = 1e30;
-    for (int b0 = 5; b0 < 5 + row_bits; ++b0)
-      for (int b1 = b0 + 1; b1 < 5 + row_bits; ++b1)
-        if (cost(b0, b1) < c2 - 1e-9) { c2 = cost(b0, b1); p0 = b0; p1 = b1; }
-    if (p0 >= 0 && c2 < 0.95 * c1) {
-      d.rb[0] = static_cast<uint8_t>(p0);
-      d.rb[1] = static_cast<uint8_t>(p1);
-    }
+// Member 0 row-invariant inside an item (no output bit in [5, cb)): the
+// kernel hoists its loads out of the row loop (DevOp::inv0).
+void mark_invariant_lead(DevOp& d, const DevTensor* ts) {
+  d.inv0 = 0;
+  if (d.ns != 1 || d.nt < 2) return;
+  for (int ax = 0; ax < ts[0].rank; ++ax) {
+    const int src = ts[0].src[ax];
+    if (src >= 5 && src < d.cb) return;
   }
+  d.inv0 = 1;
 }
 
 }  // namespace
@@ -276,7 +251,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
         hp.trefs.push_back(t);
         bytes += 16.0 * static_cast<double>(uint64_t{1} << rank);
       }
-      choose_register_bits(d, hp.trefs.data() + d.tref);
+      mark_invariant_lead(d, hp.trefs.data() + d.tref);
       hp.ops.push_back(d);
       hp.ibeg.push_back(d.item_begin);
       hp.op_width.push_back(o.record ? o.width : 0);

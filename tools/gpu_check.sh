@@ -11,6 +11,7 @@ if [ "$2" != "skip-tests" ]; then
   timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt
 fi
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/bench.err
+timeout 600 python tools/microbench.py > $O/microbench.txt 2>&1
 L=$(timeout 120 python tools/profile_step.py levels 2>/dev/null | tail -1)
 echo "levels=$L" > $O/ncu.txt
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches.csv python tools/profile_step.py step >> $O/ncu.txt 2>&1
