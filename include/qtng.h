@@ -172,7 +172,9 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
 /* Device-resident plan of ONE explicit schedule (format of qtng_edge_schedule),
  * e.g. a single wide bucket for the C3 microbenchmark.  Its initial tensor
  * data is uploaded once; qtng_plan_execute then ignores the angles and
- * returns the schedule's scalar as terms[0..1]. */
+ * returns the schedule's scalar as terms[0..1].  A schedule of exactly one
+ * bucket is planned as one ContractionBackend::contract (result kept in
+ * place, not routed). */
 qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* ints,
                                       int64_t n_ints, const double* data, int max_result_width,
                                       qtng_plan** out);

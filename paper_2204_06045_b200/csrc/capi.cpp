@@ -17,6 +17,7 @@
 #include "host.hpp"
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "pool.hpp"
 
 using namespace qtng;
 
@@ -108,6 +109,14 @@ std::vector<int> selection(int m, int n_sel, const int* sel) {
   return s;
 }
 
+// The walk the device program is built from: contract_network's symbolic
+// walk with >kMaxInputs-member buckets pre-folded.
+WalkResult device_walk(const Schedule& s, int max_width, bool route = true) {
+  WalkResult w = walk_schedule(s, max_width, route);
+  if (!w.fail_code) fold_wide_ops(w, kMaxInputs);
+  return w;
+}
+
 // Schedules + symbolic walks of the selected edges, built on host threads
 // (every lightcone is independent, like the reference's edge pool).
 struct ConeSet {
@@ -128,25 +137,13 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
       cs.edges[i] = e;
       Schedule s = edge_schedule(g, e, p);
       if (merged) s = merge_buckets(s);
-      cs.walks[i] = walk_schedule(s, max_width);
+      cs.walks[i] = device_walk(s, max_width);
     } catch (const Error& ex) {
       codes[i] = ex.code;
       errs[i] = ex.what();
     }
   };
-  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  const int nthreads = std::min(hw, k);
-  if (nthreads <= 1) {
-    for (int i = 0; i < k; ++i) work(i);
-  } else {
-    std::atomic<int> next{0};
-    std::vector<std::thread> pool;
-    for (int t = 0; t < nthreads; ++t)
-      pool.emplace_back([&] {
-        for (int i = next.fetch_add(1); i < k; i = next.fetch_add(1)) work(i);
-      });
-    for (auto& t : pool) t.join();
-  }
+  Pool::get().parallel_for(k, work);
   for (int i = 0; i < k; ++i)
     if (codes[i]) throw Error(codes[i], errs[i]);
   return cs;
@@ -357,9 +354,11 @@ qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged, d
     const ConeSet cs = plan_cones(g, p, merged != 0, 1 << 20, selection(m, m, nullptr));
     for (int i = 0; i < m; ++i) {
       double b = 0;
-      for (const Op& op : cs.walks[i].ops) {
-        b += 16.0 * static_cast<double>(uint64_t{1} << op.out_vars.size());
-        for (const OpInput& in : op.inputs) b += 16.0 * static_cast<double>(uint64_t{1} << in.vars.size());
+      const WalkResult& w = cs.walks[i];
+      for (const Op& op : w.ops) {
+        b += 16.0 * static_cast<double>(uint64_t{1} << op.r);
+        for (int t = 0; t < op.nin; ++t)
+          b += 16.0 * static_cast<double>(uint64_t{1} << w.inputs(op)[t].rank);
       }
       bytes_out[i] = b;
     }
@@ -472,10 +471,10 @@ qtng_status qtng_contract_bucket(qtng_ctx* ctx, int n_tensors, const int* ranks,
       out_data[1] = 0.0;
       return;
     }
-    const WalkResult w = walk_schedule(s, 1 << 20, /*route=*/false);
+    const WalkResult w = device_walk(s, 1 << 20, /*route=*/false);
     if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
-    const Op& op = w.ops[0];
-    const int r = static_cast<int>(op.out_vars.size());
+    const Op& op = w.ops.back();  // the bucket itself (pre-fold helpers come first)
+    const int r = op.r;
     if ((int64_t{1} << r) > out_cap) throw Error(kInvalidInput, "output buffer too small");
     const HostPlan hp = build_plan({&w}, static_cast<uint64_t>(dof));
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -486,7 +485,7 @@ qtng_status qtng_contract_bucket(qtng_ctx* ctx, int n_tensors, const int* ranks,
                               ctx->stream));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     *out_rank = r;
-    std::copy(op.out_vars.begin(), op.out_vars.end(), out_vars);
+    for (int k = 0; k < r; ++k) out_vars[k] = w.ids[w.out_vars(op)[k]];
   });
 }
 
@@ -497,7 +496,7 @@ qtng_status qtng_contract_schedule(qtng_ctx* ctx, int n_buckets, const int* ints
   return guarded([&] {
     if (!ctx) throw Error(kInvalidInput, "null context");
     const Schedule s = parse_schedule(n_buckets, ints, static_cast<long>(n_ints));
-    const WalkResult w = walk_schedule(s, max_result_width);
+    const WalkResult w = device_walk(s, max_result_width);
     if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
     uint64_t input_elems = 0;
     for (const SchedTensor& t : s.init) input_elems += uint64_t{1} << t.vars.size();
@@ -516,15 +515,15 @@ qtng_status qtng_contract_schedule(qtng_ctx* ctx, int n_buckets, const int* ints
     }
     scalar_re_im[0] = scalar.x;
     scalar_re_im[1] = scalar.y;
-    const int n = static_cast<int>(w.ops.size());
+    const int n = static_cast<int>(hp.rec_seq.size());
     if (n_records) *n_records = n;
     double total_bytes = 0;
     for (double b : hp.rec_bytes) total_bytes += b;
     for (int i = 0; i < n && i < rec_cap && records; ++i) {
       qtng_record& r = records[i];
       r.edge_u = r.edge_v = -1;
-      r.bucket_seq = w.ops[i].bucket_seq;
-      r.width = w.ops[i].width;
+      r.bucket_seq = hp.rec_seq[i];
+      r.width = hp.rec_width[i];
       r.ops = uint64_t{1} << r.width;
       r.elapsed_s = std::max(1e-9, 1e-3 * ms * (total_bytes > 0 ? hp.rec_bytes[i] / total_bytes : 0));
       r.flops_est = 8.0 * static_cast<double>(r.ops) / r.elapsed_s;
@@ -580,7 +579,9 @@ qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* i
   return guarded([&] {
     if (!ctx || !out) throw Error(kInvalidInput, "null argument");
     const Schedule s = parse_schedule(n_buckets, ints, static_cast<long>(n_ints));
-    const WalkResult w = walk_schedule(s, max_result_width);
+    // a one-bucket schedule is a single ContractionBackend::contract: its
+    // result stays in place instead of being routed
+    const WalkResult w = device_walk(s, max_result_width, /*route=*/n_buckets != 1);
     if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
     if (w.ops.empty()) throw Error(kInvalidInput, "schedule has no non-empty bucket");
     uint64_t input_elems = 0;

@@ -196,34 +196,48 @@ std::vector<int> greedy_order(const Network& net) {
   for (const InitTensor& t : net.tensors)
     for (int i = 0; i < t.rank; ++i)
       for (int j = i + 1; j < t.rank; ++j) { set(t.vars[i], t.vars[j]); set(t.vars[j], t.vars[i]); }
+  // Alive vertices bucketed by degree, one bitset per degree: the next
+  // vertex is the lowest set bit of the lowest non-empty degree bucket, i.e.
+  // minimum degree with ties to the smallest id, as the reference's std::map
+  // scan picks it.
   std::vector<int> deg(V);
+  std::vector<uint64_t> by_deg(static_cast<size_t>(V + 1) * W, 0);
+  auto bucket = [&](int d) { return by_deg.data() + static_cast<size_t>(d) * W; };
+  auto flip = [&](int d, int v) { bucket(d)[v >> 6] ^= uint64_t{1} << (v & 63); };
   for (int v = 0; v < V; ++v) {
     int c = 0;
     for (int w = 0; w < W; ++w) c += std::popcount(row(v)[w]);
     deg[v] = c;
+    flip(c, v);
   }
-  std::vector<char> alive(V, 1);
   std::vector<uint64_t> nbrs(W);
   std::vector<int> order;
   order.reserve(V);
   for (int step = 0; step < V; ++step) {
-    int best = -1, best_deg = std::numeric_limits<int>::max();
-    for (int v = 0; v < V; ++v)  // ascending id: ties go to the smallest
-      if (alive[v] && deg[v] < best_deg) { best_deg = deg[v]; best = v; }
+    int best = -1;
+    for (int d = 0; d <= V && best < 0; ++d) {
+      const uint64_t* b = bucket(d);
+      for (int w = 0; w < W; ++w)
+        if (b[w]) { best = w * 64 + std::countr_zero(b[w]); break; }
+    }
     order.push_back(best);
+    flip(deg[best], best);
     std::copy(row(best), row(best) + W, nbrs.begin());
     for (int w = 0; w < W; ++w)
       for (uint64_t bits = nbrs[w]; bits; bits &= bits - 1) {
         const int a = w * 64 + std::countr_zero(bits);
         uint64_t* ra = row(a);
         int c = 0;
-        for (int x = 0; x < W; ++x) { ra[x] |= nbrs[x]; }
+        for (int x = 0; x < W; ++x) ra[x] |= nbrs[x];
         ra[a >> 6] &= ~(uint64_t{1} << (a & 63));
         ra[best >> 6] &= ~(uint64_t{1} << (best & 63));
         for (int x = 0; x < W; ++x) c += std::popcount(ra[x]);
-        deg[a] = c;
+        if (c != deg[a]) {
+          flip(deg[a], a);
+          flip(c, a);
+          deg[a] = c;
+        }
       }
-    alive[best] = 0;
   }
   return order;
 }
@@ -263,147 +277,7 @@ Schedule edge_schedule(const Graph& g, Edge e, int p) {
 }
 
 // ---------------------------------------------------------------- symbolic walk
-
-namespace {
-
-// Dense re-indexing of the schedule's variable ids (they are arbitrary ints
-// in explicitly supplied schedules); monotone, so "ascending id" is kept.
-struct VarIndex {
-  std::vector<int> ids;  // dense -> original
-  int dense(int v) const {
-    return static_cast<int>(std::lower_bound(ids.begin(), ids.end(), v) - ids.begin());
-  }
-};
-
-VarIndex index_vars(const Schedule& s) {
-  VarIndex ix;
-  for (const SchedBucket& b : s.buckets) ix.ids.insert(ix.ids.end(), b.sum_vars.begin(), b.sum_vars.end());
-  for (const SchedTensor& t : s.init) ix.ids.insert(ix.ids.end(), t.vars.begin(), t.vars.end());
-  std::sort(ix.ids.begin(), ix.ids.end());
-  ix.ids.erase(std::unique(ix.ids.begin(), ix.ids.end()), ix.ids.end());
-  return ix;
-}
-
-struct Member {
-  bool initial;
-  int64_t ref;
-  std::vector<int> vars;  // dense ids, axis order
-};
-
-}  // namespace
-
-WalkResult walk_schedule(const Schedule& s, int max_result_width, bool route) {
-  WalkResult res;
-  const VarIndex ix = index_vars(s);
-  const int V = static_cast<int>(ix.ids.size());
-  const int B = static_cast<int>(s.buckets.size());
-  std::vector<int> pos(V, -1);  // sum_var_positions: later buckets overwrite
-  for (int i = 0; i < B; ++i)
-    for (int v : s.buckets[i].sum_vars) pos[ix.dense(v)] = i;
-  std::vector<std::vector<Member>> members(B);
-  std::vector<int> live(V, 0);  // member tensors (uncontracted) holding each var
-  for (int i = 0; i < B; ++i)
-    for (int t : s.buckets[i].tensors) {
-      Member m{true, s.init[t].data, {}};
-      for (int v : s.init[t].vars) m.vars.push_back(ix.dense(v));
-      for (int v : m.vars) ++live[v];
-      members[i].push_back(std::move(m));
-    }
-  std::vector<int> uni;
-  std::vector<char> mark(V, 0);
-  for (int i = 0; i < B; ++i) {
-    std::vector<Member>& mem = members[i];
-    if (mem.empty()) continue;
-    for (const Member& m : mem)
-      for (int v : m.vars) --live[v];
-    // liveness (engine.cpp:261-266): every member of later buckets is live
-    for (int v : s.buckets[i].sum_vars)
-      if (live[ix.dense(v)] > 0) {
-        res.fail_code = kSchedule;
-        res.fail_msg = "sum variable " + std::to_string(v) + " still live outside its bucket";
-        return res;
-      }
-    uni.clear();
-    for (const Member& m : mem)
-      for (int v : m.vars)
-        if (!mark[v]) { mark[v] = 1; uni.push_back(v); }
-    for (int v : uni) mark[v] = 0;
-    std::sort(uni.begin(), uni.end());
-    const int width = static_cast<int>(uni.size());
-    const int result_width = width - static_cast<int>(s.buckets[i].sum_vars.size());
-    if (result_width > max_result_width) {
-      res.fail_code = kResource;
-      res.fail_msg = "contraction refused: result width " + std::to_string(result_width) +
-                     " exceeds cap " + std::to_string(max_result_width);
-      return res;
-    }
-    Op op;
-    op.bucket_seq = i;
-    op.width = width;
-    for (int v : s.buckets[i].sum_vars) {
-      const int d = ix.dense(v);
-      if (!std::binary_search(uni.begin(), uni.end(), d)) {
-        res.fail_code = kSchedule;
-        res.fail_msg = "bucket sums a variable absent from its tensors";
-        return res;
-      }
-      op.sum_vars.push_back(d);
-    }
-    std::sort(op.sum_vars.begin(), op.sum_vars.end());
-    op.sum_vars.erase(std::unique(op.sum_vars.begin(), op.sum_vars.end()), op.sum_vars.end());
-    std::set_difference(uni.begin(), uni.end(), op.sum_vars.begin(), op.sum_vars.end(),
-                        std::back_inserter(op.out_vars));
-    int level = 0;
-    for (Member& m : mem) {
-      if (!m.initial) level = std::max(level, res.ops[m.ref].level + 1);
-      op.inputs.push_back(OpInput{m.initial, m.ref, std::move(m.vars)});
-    }
-    op.level = level;
-    mem.clear();
-    const int me = static_cast<int>(res.ops.size());
-    res.max_result_rank = std::max(res.max_result_rank, static_cast<int>(op.out_vars.size()));
-    if (op.out_vars.empty()) {
-      res.scalars.push_back(me);
-      res.ops.push_back(std::move(op));
-      continue;
-    }
-    if (!route) {
-      res.ops.push_back(std::move(op));
-      continue;
-    }
-    int target = std::numeric_limits<int>::max();
-    for (int v : op.out_vars) {
-      if (pos[v] < 0) {
-        res.fail_code = kSchedule;
-        res.fail_msg = "result variable not covered by the schedule";
-        return res;
-      }
-      target = std::min(target, pos[v]);
-    }
-    if (target <= i) {
-      res.fail_code = kSchedule;
-      res.fail_msg = "result tensor flows backwards in the schedule";
-      return res;
-    }
-    op.consumer = -2 - target;  // patched to the consuming op index below
-    for (int v : op.out_vars) ++live[v];
-    members[target].push_back(Member{false, me, op.out_vars});
-    res.ops.push_back(std::move(op));
-  }
-  // Resolve consumers: the op created from bucket `target` consumes.
-  std::vector<int> op_of_bucket(B, -1);
-  for (size_t k = 0; k < res.ops.size(); ++k) op_of_bucket[res.ops[k].bucket_seq] = static_cast<int>(k);
-  for (Op& op : res.ops)
-    if (op.consumer <= -2) op.consumer = op_of_bucket[-2 - op.consumer];
-  // Map dense var ids back to the schedule's ids.
-  for (Op& op : res.ops) {
-    for (int& v : op.sum_vars) v = ix.ids[v];
-    for (int& v : op.out_vars) v = ix.ids[v];
-    for (OpInput& in : op.inputs)
-      for (int& v : in.vars) v = ix.ids[v];
-  }
-  return res;
-}
+// walk_schedule / fold_wide_ops: walk.cpp
 
 std::vector<int> simulate_widths(const Schedule& s) {
   const WalkResult w = walk_schedule(s, std::numeric_limits<int>::max());

@@ -126,30 +126,51 @@ Schedule merge_buckets(const Schedule& s);
 // One non-empty bucket of a lightcone, contracted.  Inputs are listed in the
 // bucket's member order: initial tensors in network order, then results in
 // production order (the routing of contract_network, engine.cpp:286-301).
-struct OpInput {
-  bool initial = true;
-  int64_t ref = 0;          // initial: data offset in input region; else producer op index
-  std::vector<int> vars;    // axis order of that tensor (MSB first)
+// Flat storage: every var list lives in WalkResult::vars as DENSE ids
+// (0..n_vars-1, ascending order preserved); WalkResult::ids maps them back.
+struct OpIn {
+  int64_t ref;       // initial: element offset in the input region; else producer op index
+  int32_t var_off;   // axis vars (MSB first) at vars[var_off .. var_off+rank)
+  int16_t rank;
+  uint8_t initial;
+  uint8_t pad;
 };
 
 struct Op {
-  int bucket_seq = 0;          // schedule index of the bucket (TimingRecord.bucket_seq)
-  int width = 0;               // |union of vars| (TimingRecord.width)
-  std::vector<int> sum_vars;   // sorted, present
-  std::vector<int> out_vars;   // ascending (the result's axes)
-  std::vector<OpInput> inputs;
-  int consumer = -1;           // op consuming the result, -1 => scalar
-  int level = 0;               // dependency depth (0 = only initial inputs)
+  int32_t bucket_seq;  // schedule index of the bucket (TimingRecord.bucket_seq)
+  int32_t width;       // |union of vars| (TimingRecord.width)
+  int32_t level;       // dependency depth (0 = only initial inputs)
+  int32_t consumer;    // op consuming the result, -1 => scalar (or kept in place)
+  int32_t sum_off;     // sorted summed vars at vars[sum_off .. sum_off+ns)
+  int32_t out_off;     // ascending result vars at vars[out_off .. out_off+r)
+  int32_t in_off;      // inputs at ins[in_off .. in_off+nin)
+  int16_t ns, r;
+  int32_t nin;
 };
 
 struct WalkResult {
   std::vector<Op> ops;         // in schedule (execution) order
+  std::vector<OpIn> ins;
+  std::vector<int32_t> vars;   // dense var ids
+  std::vector<int32_t> ids;    // dense -> schedule var id
+  int n_vars = 0;
   std::vector<int> scalars;    // ops with empty results, in production order
   int max_result_rank = 0;     // peak_tensor_bytes = 16 << max_result_rank
   // contract_network failure, if any (code, message); ops before it are valid
   int fail_code = 0;
   std::string fail_msg;
+
+  const int32_t* out_vars(const Op& o) const { return vars.data() + o.out_off; }
+  const int32_t* sum_vars(const Op& o) const { return vars.data() + o.sum_off; }
+  const OpIn* inputs(const Op& o) const { return ins.data() + o.in_off; }
+  const int32_t* in_vars(const OpIn& i) const { return vars.data() + i.var_off; }
 };
+
+// Replace every op with more than kMaxInputs members by a chain of pre-fold
+// helper ops (the product of the first kMaxInputs members over their joint
+// vars, no summation).  prod = (1*P)*T8*... rounds exactly like the
+// reference's left fold ((1*T0)*T1)*...*T8*...  Helper ops get bucket_seq -1.
+void fold_wide_ops(WalkResult& w, int max_inputs);
 
 // The data-free contract_network walk (engine.cpp:246-304, including the
 // liveness check :261-266 and contract_bucket's cap check :160-169).

@@ -1,97 +1,21 @@
 // Offline planner: turns per-lightcone symbolic walks into one level-
-// synchronous device program (see plan.hpp / device_plan.hpp).
+// synchronous device program (see plan.hpp / device_plan.hpp).  Linear-time
+// passes over flat arrays: counting sorts by level, O(1) size-class arena
+// allocation, stamp-array bit maps.
 #include "plan.hpp"
 
 #include <algorithm>
-#include <map>
-#include <set>
+
+#include "pool.hpp"
 
 namespace qtng {
 
 namespace {
 
 constexpr uint64_t kAlign = 32;  // elements (512 B)
+constexpr int kMinClass = 5;     // results are allocated in 2^max(r,5) blocks
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
-
-// Best-fit allocator with coalescing over arena element offsets.
-class Arena {
- public:
-  explicit Arena(uint64_t base) : top_(base), peak_(base) {}
-  uint64_t alloc(uint64_t n) {
-    auto it = by_size_.lower_bound({n, 0});
-    if (it != by_size_.end()) {
-      const auto [size, off] = *it;
-      by_size_.erase(it);
-      by_off_.erase(off);
-      if (size > n) insert_free(off + n, size - n);
-      return off;
-    }
-    // grow: absorb a free block that ends at the top
-    if (!by_off_.empty()) {
-      auto last = std::prev(by_off_.end());
-      if (last->first + last->second == top_) {
-        const uint64_t off = last->first;
-        by_size_.erase({last->second, off});
-        by_off_.erase(last);
-        top_ = off + n;
-        peak_ = std::max(peak_, top_);
-        return off;
-      }
-    }
-    const uint64_t off = top_;
-    top_ += n;
-    peak_ = std::max(peak_, top_);
-    return off;
-  }
-  void release(uint64_t off, uint64_t n) {
-    auto next = by_off_.lower_bound(off);
-    if (next != by_off_.end() && off + n == next->first) {
-      by_size_.erase({next->second, next->first});
-      n += next->second;
-      next = by_off_.erase(next);
-    }
-    if (next != by_off_.begin()) {
-      auto prev = std::prev(next);
-      if (prev->first + prev->second == off) {
-        by_size_.erase({prev->second, prev->first});
-        off = prev->first;
-        n += prev->second;
-        by_off_.erase(prev);
-      }
-    }
-    insert_free(off, n);
-  }
-  uint64_t peak() const { return peak_; }
-
- private:
-  void insert_free(uint64_t off, uint64_t n) {
-    by_off_[off] = n;
-    by_size_.insert({n, off});
-  }
-  uint64_t top_, peak_;
-  std::map<uint64_t, uint64_t> by_off_;
-  std::set<std::pair<uint64_t, uint64_t>> by_size_;
-};
-
-struct GIn {
-  bool initial;
-  int64_t ref;  // initial: input-region offset; else global op index
-  std::vector<int> vars;
-};
-
-struct GOp {
-  int lc = 0;
-  bool record = true;  // false for pre-fold helpers
-  int width = 0;
-  std::vector<int> sum_vars, out_vars;
-  std::vector<GIn> ins;
-  int level = 0;
-  int consumer = -1;   // global op index, -1 scalar
-  uint64_t out = 0;
-};
-
-uint64_t out_alloc_size(int r) { return round_up(uint64_t{1} << r, kAlign); }
 
 // Member 0 row-invariant inside an item (no output bit in [5, cb)): the
 // kernel hoists its loads out of the row loop (DevOp::inv0).
@@ -105,180 +29,207 @@ void mark_invariant_lead(DevOp& d, const DevTensor* ts) {
   d.inv0 = 1;
 }
 
+// Power-of-two size classes; a class's freed blocks are reused first-in
+// last-out, fresh blocks come from the top.  Result lifetimes are level
+// intervals, so reuse is dense and the peak stays near the live maximum.
+class ClassArena {
+ public:
+  explicit ClassArena(uint64_t base) : top_(base) {}
+  uint64_t alloc(int cls) {
+    if (cls < static_cast<int>(free_.size()) && !free_[cls].empty()) {
+      const uint64_t off = free_[cls].back();
+      free_[cls].pop_back();
+      return off;
+    }
+    const uint64_t off = top_;
+    top_ += uint64_t{1} << cls;
+    return off;
+  }
+  void release(int cls, uint64_t off) {
+    if (cls >= static_cast<int>(free_.size())) free_.resize(cls + 1);
+    free_[cls].push_back(off);
+  }
+  uint64_t peak() const { return top_; }
+
+ private:
+  uint64_t top_;
+  std::vector<std::vector<uint64_t>> free_;
+};
+
 }  // namespace
 
 HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems) {
   HostPlan hp;
   hp.input_elems = input_elems;
-  std::vector<GOp> g;
-  std::vector<std::vector<int>> cone_scalars(cones.size());
-  hp.rec_begin.push_back(0);
-  size_t total = 0;
-  for (const WalkResult* w : cones) total += w->ops.size();
-  g.reserve(total + total / 8);
-
-  for (size_t c = 0; c < cones.size(); ++c) {
-    const WalkResult& w = *cones[c];
-    std::vector<int> gid(w.ops.size());
-    for (size_t k = 0; k < w.ops.size(); ++k) {
-      const Op& op = w.ops[k];
-      std::vector<GIn> ins;
-      ins.reserve(op.inputs.size());
-      for (const OpInput& in : op.inputs)
-        ins.push_back(GIn{in.initial, in.initial ? in.ref : gid[in.ref], in.vars});
-      // Pre-fold wide member lists: the product of the first kMaxInputs members
-      // over their joint vars, no summation.  prod = (1*P)*T8*... rounds
-      // exactly like the reference's left fold ((1*T0)*T1)*...*T8*...
-      while (ins.size() > static_cast<size_t>(kMaxInputs)) {
-        GOp f;
-        f.lc = static_cast<int>(c);
-        f.record = false;
-        for (int t = 0; t < kMaxInputs; ++t)
-          f.out_vars.insert(f.out_vars.end(), ins[t].vars.begin(), ins[t].vars.end());
-        std::sort(f.out_vars.begin(), f.out_vars.end());
-        f.out_vars.erase(std::unique(f.out_vars.begin(), f.out_vars.end()), f.out_vars.end());
-        f.width = static_cast<int>(f.out_vars.size());
-        f.ins.assign(ins.begin(), ins.begin() + kMaxInputs);
-        const int fid = static_cast<int>(g.size());
-        GIn folded{false, fid, f.out_vars};
-        g.push_back(std::move(f));
-        ins.erase(ins.begin(), ins.begin() + kMaxInputs);
-        ins.insert(ins.begin(), std::move(folded));
-      }
-      GOp o;
-      o.lc = static_cast<int>(c);
-      o.width = op.width;
-      o.sum_vars = op.sum_vars;
-      o.out_vars = op.out_vars;
-      o.ins = std::move(ins);
-      gid[k] = static_cast<int>(g.size());
-      g.push_back(std::move(o));
-      // records (one per non-empty bucket, schedule order)
-      hp.rec_seq.push_back(op.bucket_seq);
-      hp.rec_width.push_back(op.width);
+  const int C = static_cast<int>(cones.size());
+  std::vector<uint32_t> base(C + 1, 0);
+  int max_vars = 0;
+  for (int c = 0; c < C; ++c) {
+    base[c + 1] = base[c] + static_cast<uint32_t>(cones[c]->ops.size());
+    max_vars = std::max(max_vars, cones[c]->n_vars);
+    hp.max_result_rank = std::max(hp.max_result_rank, cones[c]->max_result_rank);
+  }
+  const uint32_t N = base[C];
+  std::vector<uint32_t> lc_of(N);
+  int max_level = -1;
+  for (int c = 0; c < C; ++c)
+    for (uint32_t k = 0; k < cones[c]->ops.size(); ++k) {
+      const Op& o = cones[c]->ops[k];
+      if (o.nin > kMaxInputs) throw Error(kSchedule, "internal: op not pre-folded");
+      if (o.ns > kMaxSumBits)
+        throw Error(kInvalidInput, "bucket sums " + std::to_string(o.ns) +
+                                       " variables; the device path supports at most " +
+                                       std::to_string(kMaxSumBits));
+      lc_of[base[c] + k] = c;
+      max_level = std::max(max_level, static_cast<int>(o.level));
     }
-    for (int s : w.scalars) cone_scalars[c].push_back(gid[s]);
-    hp.rec_begin.push_back(static_cast<uint32_t>(hp.rec_seq.size()));
-    hp.max_result_rank = std::max(hp.max_result_rank, w.max_result_rank);
+  const int n_levels = max_level + 1;
+  auto op_at = [&](uint32_t g) -> const Op& { return cones[lc_of[g]]->ops[g - base[lc_of[g]]]; };
+
+  // stable counting sort by level; release lists by consumer level
+  std::vector<uint32_t> lstart(n_levels + 1, 0), order(N);
+  std::vector<uint32_t> rstart(n_levels + 1, 0), rel;
+  std::vector<uint64_t> level_rows(n_levels, 0);
+  for (uint32_t g = 0; g < N; ++g) {
+    const Op& o = op_at(g);
+    ++lstart[o.level + 1];
+    level_rows[o.level] += o.r > 5 ? uint64_t{1} << (o.r - 5) : 1;
+    if (o.consumer >= 0) ++rstart[cones[lc_of[g]]->ops[o.consumer].level + 1];
+  }
+  for (int L = 0; L < n_levels; ++L) {
+    lstart[L + 1] += lstart[L];
+    rstart[L + 1] += rstart[L];
+  }
+  rel.resize(rstart[n_levels]);
+  {
+    std::vector<uint32_t> lf(lstart.begin(), lstart.end() - 1), rf(rstart.begin(), rstart.end() - 1);
+    for (uint32_t g = 0; g < N; ++g) {
+      const Op& o = op_at(g);
+      order[lf[o.level]++] = g;
+      if (o.consumer >= 0) rel[rf[cones[lc_of[g]]->ops[o.consumer].level]++] = g;
+    }
   }
 
-  // levels + consumers
-  int max_level = 0;
-  for (size_t i = 0; i < g.size(); ++i) {
-    int lv = 0;
-    for (const GIn& in : g[i].ins)
-      if (!in.initial) {
-        lv = std::max(lv, g[in.ref].level + 1);
-        g[in.ref].consumer = static_cast<int>(i);
-      }
-    g[i].level = lv;
-    max_level = std::max(max_level, lv);
-  }
-  const int n_levels = g.empty() ? 0 : max_level + 1;
-
-  // stable level sort
-  std::vector<std::vector<int>> by_level(n_levels);
-  for (size_t i = 0; i < g.size(); ++i) by_level[g[i].level].push_back(static_cast<int>(i));
-
-  // arena placement over level lifetimes; scalars live to the end
-  Arena arena(round_up(input_elems, kAlign));
-  std::vector<std::vector<int>> release(n_levels + 1);
+  // arena placement over level lifetimes; scalars / kept results live to the end
+  std::vector<uint64_t> out(N);
+  ClassArena arena(round_up(input_elems, kAlign));
+  auto cls_of = [&](uint32_t g) { return std::max<int>(op_at(g).r, kMinClass); };
   for (int L = 0; L < n_levels; ++L) {
     if (L > 0)
-      for (int i : release[L - 1]) arena.release(g[i].out, out_alloc_size(static_cast<int>(g[i].out_vars.size())));
-    for (int i : by_level[L]) {
-      g[i].out = arena.alloc(out_alloc_size(static_cast<int>(g[i].out_vars.size())));
-      if (g[i].consumer >= 0) release[g[g[i].consumer].level].push_back(i);
-    }
+      for (uint32_t i = rstart[L - 1]; i < rstart[L]; ++i) arena.release(cls_of(rel[i]), out[rel[i]]);
+    for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) out[order[i]] = arena.alloc(cls_of(order[i]));
   }
   hp.arena_elems = arena.peak();
 
-  // descriptors
-  hp.ops.reserve(g.size());
+  // descriptors, level by level: the item/tref prefix sums sequentially ...
+  hp.ops.resize(N);
+  hp.ibeg.resize(N);
+  hp.op_width.resize(N);
   hp.level_bytes.assign(n_levels, 0.0);
+  std::vector<double> op_bytes(N);
+  uint32_t n_trefs = 0;
   for (int L = 0; L < n_levels; ++L) {
-    LevelLaunch ll{static_cast<uint32_t>(hp.ops.size()), 0, 0, 0};
+    LevelLaunch ll{lstart[L], lstart[L + 1] - lstart[L], 0, 0};
     // item size: 32-output rows per warp item, fewer for small levels so the
     // level still spreads over the whole GPU
-    uint64_t level_rows = 0;
-    for (int i : by_level[L]) {
-      const int r = static_cast<int>(g[i].out_vars.size());
-      level_rows += r > 5 ? uint64_t{1} << (r - 5) : 1;
-    }
     int row_bits = 0;
-    while (row_bits < kItemBits - 5 && (level_rows >> (row_bits + 1)) >= kTargetItems) ++row_bits;
-    for (int i : by_level[L]) {
-      const GOp& o = g[i];
-      const int r = static_cast<int>(o.out_vars.size());
-      const int ns = static_cast<int>(o.sum_vars.size());
-      if (ns > kMaxSumBits)
-        throw Error(kInvalidInput, "bucket sums " + std::to_string(ns) +
-                                       " variables; the device path supports at most " +
-                                       std::to_string(kMaxSumBits));
-      DevOp d{};
-      d.out = o.out;
+    while (row_bits < kItemBits - 5 && (level_rows[L] >> (row_bits + 1)) >= kTargetItems) ++row_bits;
+    for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) {
+      const Op& o = op_at(order[i]);
+      DevOp& d = hp.ops[i];
+      d.out = out[order[i]];
       d.item_begin = ll.items;
-      d.tref = static_cast<uint32_t>(hp.trefs.size());
-      d.r = static_cast<uint8_t>(r);
-      d.ns = static_cast<uint8_t>(ns);
-      d.nt = static_cast<uint8_t>(o.ins.size());
-      d.cb = static_cast<uint8_t>(std::min(r, 5 + row_bits));
+      d.tref = n_trefs;
+      d.r = static_cast<uint8_t>(o.r);
+      d.ns = static_cast<uint8_t>(o.ns);
+      d.nt = static_cast<uint8_t>(o.nin);
+      d.cb = static_cast<uint8_t>(std::min<int>(o.r, 5 + row_bits));
       ll.max_nt = std::max<uint32_t>(ll.max_nt, d.nt);
-      const uint64_t items = uint64_t{1} << (r - d.cb);
+      const uint64_t items = uint64_t{1} << (o.r - d.cb);
       if (ll.items + items > 0xffffffffull) throw Error(kResource, "level has too many work items");
       ll.items += static_cast<uint32_t>(items);
-      double bytes = 16.0 * static_cast<double>(uint64_t{1} << r);
-      for (const GIn& in : o.ins) {
-        const int rank = static_cast<int>(in.vars.size());
-        if (rank > kMaxRank)
-          throw Error(kResource, "tensor rank " + std::to_string(rank) +
-                                     " exceeds the device limit " + std::to_string(kMaxRank));
-        DevTensor t{};
-        t.off = in.initial ? static_cast<uint64_t>(in.ref) : g[in.ref].out;
-        t.rank = static_cast<uint8_t>(rank);
-        for (int ax = 0; ax < rank; ++ax) {
-          const int v = in.vars[ax];
-          auto ko = std::lower_bound(o.out_vars.begin(), o.out_vars.end(), v);
-          if (ko != o.out_vars.end() && *ko == v) {
-            t.src[ax] = static_cast<uint8_t>(r - 1 - (ko - o.out_vars.begin()));
-          } else {
-            auto ks = std::lower_bound(o.sum_vars.begin(), o.sum_vars.end(), v);
-            if (ks == o.sum_vars.end() || *ks != v)
-              throw Error(kSchedule, "internal: operand var outside its bucket");
-            t.src[ax] = static_cast<uint8_t>(kSumSrc + (ns - 1 - (ks - o.sum_vars.begin())));
-          }
-        }
-        hp.trefs.push_back(t);
-        bytes += 16.0 * static_cast<double>(uint64_t{1} << rank);
-      }
-      mark_invariant_lead(d, hp.trefs.data() + d.tref);
-      hp.ops.push_back(d);
-      hp.ibeg.push_back(d.item_begin);
-      hp.op_width.push_back(o.record ? o.width : 0);
-      ++ll.op_count;
-      hp.level_bytes[L] += bytes;
-      hp.alg_bytes += bytes;
-      if (o.record) {
-        hp.sum_ops += static_cast<double>(uint64_t{1} << o.width);
-        ++hp.n_buckets;
-        hp.max_width = std::max(hp.max_width, o.width);
-      }
+      hp.ibeg[i] = d.item_begin;
+      hp.op_width[i] = o.bucket_seq >= 0 ? o.width : 0;
+      n_trefs += static_cast<uint32_t>(o.nin);
     }
     hp.levels.push_back(ll);
   }
-  // record levels / bytes (records follow the walk order of each cone)
-  hp.rec_level.reserve(hp.rec_seq.size());
-  for (const GOp& o : g)
-    if (o.record) {
-      double bytes = 16.0 * static_cast<double>(uint64_t{1} << o.out_vars.size());
-      for (const GIn& in : o.ins) bytes += 16.0 * static_cast<double>(uint64_t{1} << in.vars.size());
-      hp.rec_level.push_back(o.level);
-      hp.rec_bytes.push_back(bytes);
-      hp.rec_out.push_back(o.out);
+  // ... then every operand's bit map in parallel chunks
+  hp.trefs.resize(n_trefs);
+  const int chunks = static_cast<int>(std::min<uint32_t>(N, 256));
+  std::vector<int> chunk_err(chunks, 0);
+  Pool::get().parallel_for(chunks, [&](int ch) {
+    const uint32_t i0 = static_cast<uint32_t>(uint64_t{N} * ch / chunks);
+    const uint32_t i1 = static_cast<uint32_t>(uint64_t{N} * (ch + 1) / chunks);
+    std::vector<uint8_t> pm(max_vars);
+    std::vector<uint32_t> pm_stamp(max_vars, ~0u);
+    for (uint32_t i = i0; i < i1; ++i) {
+      const uint32_t g = order[i];
+      const WalkResult& w = *cones[lc_of[g]];
+      const Op& o = op_at(g);
+      const uint32_t cb0 = base[lc_of[g]];
+      DevOp& d = hp.ops[i];
+      const int r = o.r, ns = o.ns;
+      // output var -> bit (LSB-indexed), summed var -> kSumSrc + j
+      const int32_t* ov = w.out_vars(o);
+      const int32_t* sv = w.sum_vars(o);
+      for (int k = 0; k < r; ++k) { pm[ov[k]] = static_cast<uint8_t>(r - 1 - k); pm_stamp[ov[k]] = g; }
+      for (int k = 0; k < ns; ++k) { pm[sv[k]] = static_cast<uint8_t>(kSumSrc + ns - 1 - k); pm_stamp[sv[k]] = g; }
+      double bytes = 16.0 * static_cast<double>(uint64_t{1} << r);
+      const OpIn* ins = w.inputs(o);
+      for (int t = 0; t < o.nin; ++t) {
+        const OpIn& in = ins[t];
+        if (in.rank > kMaxRank) { chunk_err[ch] = 1; return; }
+        DevTensor& x = hp.trefs[d.tref + t];
+        x = DevTensor{};
+        x.off = in.initial ? static_cast<uint64_t>(in.ref) : out[cb0 + in.ref];
+        x.rank = static_cast<uint8_t>(in.rank);
+        const int32_t* iv = w.in_vars(in);
+        for (int ax = 0; ax < in.rank; ++ax) {
+          if (pm_stamp[iv[ax]] != g) { chunk_err[ch] = 2; return; }
+          x.src[ax] = pm[iv[ax]];
+        }
+        bytes += 16.0 * static_cast<double>(uint64_t{1} << in.rank);
+      }
+      mark_invariant_lead(d, hp.trefs.data() + d.tref);
+      op_bytes[g] = bytes;
     }
+  });
+  for (int e : chunk_err) {
+    if (e == 1) throw Error(kResource, "tensor rank exceeds the device limit " + std::to_string(kMaxRank));
+    if (e == 2) throw Error(kSchedule, "internal: operand var outside its bucket");
+  }
+  for (int L = 0; L < n_levels; ++L)
+    for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) {
+      const uint32_t g = order[i];
+      const Op& o = op_at(g);
+      hp.level_bytes[L] += op_bytes[g];
+      hp.alg_bytes += op_bytes[g];
+      if (o.bucket_seq >= 0) {
+        hp.sum_ops += static_cast<double>(uint64_t{1} << o.width);
+        ++hp.n_buckets;
+        hp.max_width = std::max(hp.max_width, static_cast<int>(o.width));
+      }
+    }
+
+  // records (one per non-empty bucket, walk order) and per-lightcone scalars
+  hp.rec_begin.reserve(C + 1);
+  hp.rec_begin.push_back(0);
+  hp.lc_begin.reserve(C + 1);
   hp.lc_begin.push_back(0);
-  for (const auto& sc : cone_scalars) {
-    for (int i : sc) hp.scalar_off.push_back(g[i].out);
+  for (int c = 0; c < C; ++c) {
+    const WalkResult& w = *cones[c];
+    for (uint32_t k = 0; k < w.ops.size(); ++k) {
+      const Op& o = w.ops[k];
+      if (o.bucket_seq < 0) continue;
+      hp.rec_seq.push_back(o.bucket_seq);
+      hp.rec_width.push_back(o.width);
+      hp.rec_level.push_back(o.level);
+      hp.rec_bytes.push_back(op_bytes[base[c] + k]);
+      hp.rec_out.push_back(out[base[c] + k]);
+    }
+    hp.rec_begin.push_back(static_cast<uint32_t>(hp.rec_seq.size()));
+    for (int s : w.scalars) hp.scalar_off.push_back(out[base[c] + s]);
     hp.lc_begin.push_back(static_cast<uint32_t>(hp.scalar_off.size()));
   }
   return hp;
