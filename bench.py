@@ -53,6 +53,19 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def committed_traffic():
+    """DRAM read+write bytes per step of the level kernel, from the newest
+    committed ncu launch list (profiles/<tag>/traffic.json, written by
+    tools/summarize_profiles.py) -- ncu numbers are never measured here."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")))
+    if not files:
+        return {"traffic": None}
+    with open(files[-1]) as f:
+        t = json.load(f)
+    return {"traffic": t["level_kernel_dram_bytes_per_step"], "traffic_source": t["source"]}
+
+
 def golden_energy(name):
     try:
         with open(os.path.join(ROOT, "tests", "golden", "energies.json")) as f:
@@ -284,7 +297,7 @@ def run_b200(args, cfg):
         "roofline": {"bound": "hbm", "kernel": "level_kernel (all levels)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "peak_source": peak_kind, "traffic": None,
+                     "peak_source": peak_kind, **committed_traffic(),
                      "alg_bytes_per_step": info.alg_bytes,
                      "level_kernel_ms_per_step": lvl_kernel_ms},
         "roofline_largest_level": {"level": big_level, "alg_bytes": big_bytes, "ms": big_ms,

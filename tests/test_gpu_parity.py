@@ -214,3 +214,20 @@ def test_edge_subset_and_sharded_energy(q, ctx, golden):
         t = q.Plan(g, 4, edges=s, ctx=ctx).execute(a)
         full += dist.scatter_terms(g.m, s, t)
     assert dist.energy_from_terms(g.m, full) == c["energy_naive"]
+
+
+def test_merged_schedules_match_reference(q, ctx, golden):
+    # acceptance.cpp criterion 3 (merged vs unmerged at 1e-10), merged buckets
+    # summing several vars through the multi-sum kernel path
+    n_checked = 0
+    for rec in golden["acceptance"]:
+        if "energy_merged" not in rec:
+            continue
+        g = q.random_regular(rec["n"], 3, rec["seed"])
+        res = q.energy_expectation(g, q.Angles(rec["gammas"], rec["betas"]), q.GpuBackend(ctx),
+                                   merged=True)
+        scale = max(1.0, abs(rec["energy_merged"]))
+        assert abs(res.energy - rec["energy_merged"]) / scale <= 1e-10, rec["name"]
+        assert abs(res.energy - rec["energy_naive"]) / scale <= 1e-10, rec["name"]
+        n_checked += 1
+    assert n_checked >= 10
