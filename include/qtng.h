@@ -124,7 +124,8 @@ qtng_status qtng_validate_energy(int n, int m, const int* edges, int p, int merg
 /* Host-only dump of the device program for the selected edges (sel = NULL:
  * all), for analysis and tests.  Per device op (level-sorted), 8 ints:
  *   level, r (result rank), ns (summed bits), nt (inputs), cb (log2 outputs
- *   per work item), recorded (0 for a pre-fold helper), width, 0
+ *   per work item), recorded (0 for a pre-fold helper), width, outer (1 when
+ *   the op runs in the outer-join kernel)
  * then per input 34 ints: rank, initial (1 = gate/input-region tensor),
  *   src[32] (kMaxRank axis sources; <64 output bit, >=64 summed bit 64+j).
  * *n_ints receives the size needed; nothing is written if cap is short. */

@@ -394,14 +394,15 @@ def plan_dump(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfig
                               buf, len(buf), C.byref(n_ints), C.byref(n_ops)))
     out, i = [], 0
     for _ in range(n_ops.value):
-        lv, r, ns, nt, cb, rec, w, _z = (int(x) for x in buf[i:i + 8])
+        lv, r, ns, nt, cb, rec, w, outer = (int(x) for x in buf[i:i + 8])
         i += 8
         ins = []
         for _ in range(nt):
             rank, init = int(buf[i]), int(buf[i + 1])
             ins.append((rank, init, [int(x) for x in buf[i + 2:i + 2 + rank]]))
             i += 34
-        out.append(dict(level=lv, r=r, ns=ns, nt=nt, cb=cb, recorded=rec, width=w, inputs=ins))
+        out.append(dict(level=lv, r=r, ns=ns, nt=nt, cb=cb, recorded=rec, width=w, outer=outer,
+                        inputs=ins))
     return out
 
 

@@ -189,7 +189,8 @@ struct qtng_ctx {
   uint64_t arena_gen = 0;
   DevBuf desc;           // scratch descriptors (one-shot calls)
   PinBuf pin_desc, pin_in, pin_out;
-  DevBuf flush;          // L2 flush scratch
+  cudaStream_t stream2 = nullptr;  // outer-join kernels, forked per level
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   void ensure_arena(uint64_t elems) {
@@ -220,16 +221,41 @@ struct DevProgram {
   double2* terms() const { return reinterpret_cast<double2*>(base + L.terms); }
 };
 
-// Enqueue the whole program on `s`: every level, then the per-lightcone products.
-void enqueue_program(cudaStream_t s, const HostPlan& hp, const DevProgram& pr, double2* arena,
+// One level: the outer-join kernel forked onto the side stream, the generic
+// kernel on the main stream, joined before the next level.
+void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, const DevProgram& pr, double2* arena) {
+  const bool fork = lv.outer_items > 0;
+  if (fork) {
+    QTNG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+    QTNG_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->fork_ev, 0));
+    QTNG_CUDA(launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+    QTNG_CUDA(cudaEventRecord(ctx->join_ev, ctx->stream2));
+  }
+  QTNG_CUDA(launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+  if (fork) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+}
+
+// Enqueue the whole program on the context's stream: every level, then the
+// per-lightcone products.
+void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, double2* arena,
                      std::vector<cudaEvent_t>* level_events) {
+  cudaStream_t s = ctx->stream;
   for (size_t L = 0; L < hp.levels.size(); ++L) {
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
-    QTNG_CUDA(launch_level(s, pr.ops(), pr.ibeg(), pr.trefs(), arena, hp.levels[L]));
+    enqueue_level(ctx, hp.levels[L], pr, arena);
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
   QTNG_CUDA(launch_final(s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
                          arena, pr.terms()));
+}
+
+int launches_per_run(const HostPlan& hp) {
+  int lv = 0, outer = 0;
+  for (const LevelLaunch& l : hp.levels) {
+    lv += l.items > 0;
+    outer += l.outer_items > 0;
+  }
+  return kernels_per_plan(lv, outer);
 }
 
 // Ops of the reference's run_edge post-processing (engine.cpp:517-519, 543-546).
@@ -278,8 +304,11 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
     ctx->device = device;
     QTNG_CUDA(cudaSetDevice(device));
     QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
     QTNG_CUDA(cudaEventCreate(&ctx->ev0));
     QTNG_CUDA(cudaEventCreate(&ctx->ev1));
+    QTNG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    QTNG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     if (arena_bytes) ctx->ensure_arena(arena_bytes / sizeof(double2));
     *out = ctx.release();
   });
@@ -289,11 +318,13 @@ void qtng_destroy(qtng_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
-  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
-  cudaStream_t s = ctx->stream;
+  cudaStreamSynchronize(ctx->stream2);
+  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev})
+    if (e) cudaEventDestroy(e);
+  cudaStream_t s = ctx->stream, s2 = ctx->stream2;
   delete ctx;  // frees the arena and staging buffers
   if (s) cudaStreamDestroy(s);
+  if (s2) cudaStreamDestroy(s2);
 }
 
 qtng_status qtng_random_regular(int n, int d, uint64_t seed, int* edges, int cap, int* m_out) {
@@ -393,11 +424,12 @@ qtng_status qtng_plan_dump(int n, int m, const int* edges, int p, int merged,
     const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems);
     std::vector<int> out;
     for (size_t L = 0; L < hp.levels.size(); ++L)
-      for (uint32_t k = 0; k < hp.levels[L].op_count; ++k) {
+      for (uint32_t k = 0; k < hp.levels[L].op_count + hp.levels[L].outer_count; ++k) {
         const uint32_t i = hp.levels[L].op_begin + k;
         const DevOp& d = hp.ops[i];
+        const int outer = k >= hp.levels[L].op_count ? 1 : 0;
         out.insert(out.end(), {static_cast<int>(L), d.r, d.ns, d.nt, d.cb,
-                               hp.op_width[i] > 0 ? 1 : 0, hp.op_width[i], 0});
+                               hp.op_width[i] > 0 ? 1 : 0, hp.op_width[i], outer});
         for (int t = 0; t < d.nt; ++t) {
           const DevTensor& x = hp.trefs[d.tref + t];
           out.push_back(x.rank);
@@ -431,7 +463,7 @@ void run_program_once(qtng_ctx* ctx, const HostPlan& hp, const double* input,
   QTNG_CUDA(cudaMemcpyAsync(ctx->desc.p, ctx->pin_desc.p, L.total, cudaMemcpyHostToDevice,
                             ctx->stream));
   DevProgram pr{static_cast<char*>(ctx->desc.p), L};
-  enqueue_program(ctx->stream, hp, pr, ctx->A(), nullptr);
+  enqueue_program(ctx, hp, pr, ctx->A(), nullptr);
   if (terms_host) {
     const size_t nb = (hp.lc_begin.size() - 1) * sizeof(double2);
     QTNG_CUDA(cudaMemcpyAsync(terms_host, pr.terms(), nb, cudaMemcpyDeviceToHost, ctx->stream));
@@ -627,7 +659,7 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     QTNG_CUDA(cudaMemcpyAsync(ctx->A(), plan->pin_gate.p, hp.input_elems * sizeof(double2),
                               cudaMemcpyHostToDevice, ctx->stream));
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    enqueue_program(ctx->stream, hp, plan->prog, ctx->A(), &plan->lev_ev);
+    enqueue_program(ctx, hp, plan->prog, ctx->A(), &plan->lev_ev);
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     const size_t nb = plan->edges.size() * sizeof(double2);
     QTNG_CUDA(cudaMemcpyAsync(plan->pin_terms.p, plan->prog.terms(), nb, cudaMemcpyDeviceToHost,
@@ -657,7 +689,7 @@ qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms) 
       plan->graph = nullptr;
       cudaGraph_t gr = nullptr;
       QTNG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      enqueue_program(ctx->stream, hp, plan->prog, ctx->A(), nullptr);
+      enqueue_program(ctx, hp, plan->prog, ctx->A(), nullptr);
       QTNG_CUDA(cudaStreamEndCapture(ctx->stream, &gr));
       QTNG_CUDA(cudaGraphInstantiate(&plan->graph, gr, 0));
       cudaGraphDestroy(gr);
@@ -687,7 +719,7 @@ qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info) {
     info->sum_ops = hp.sum_ops;
     info->arena_bytes = hp.arena_elems * sizeof(double2);
     info->desc_bytes = plan->prog.L.total;
-    info->kernels_per_run = kernels_per_plan(static_cast<int>(hp.levels.size()));
+    info->kernels_per_run = launches_per_run(hp);
   });
 }
 
@@ -745,12 +777,9 @@ qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* le
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     ctx->ensure_arena(hp.arena_elems);
-    QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.ibeg(), plan->prog.trefs(), ctx->A(),
-                           hp.levels[level]));  // warm-up
+    enqueue_level(ctx, hp.levels[level], plan->prog, ctx->A());  // warm-up
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    for (int i = 0; i < n_runs; ++i)
-      QTNG_CUDA(launch_level(ctx->stream, plan->prog.ops(), plan->prog.ibeg(), plan->prog.trefs(), ctx->A(),
-                             hp.levels[level]));
+    for (int i = 0; i < n_runs; ++i) enqueue_level(ctx, hp.levels[level], plan->prog, ctx->A());
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;

@@ -37,7 +37,13 @@ struct alignas(16) DevOp {
   // in [5, cb), e.g. the gate on the summed variable): the kernel then loads
   // it once per item instead of once per row.  Only set for ns == 1, nt >= 2.
   uint8_t inv0;
-  uint8_t pad[3];
+  // Outer-join ops (run by outer_kernel): members [0, lead) are row-invariant
+  // gates, member lead = "A", member lead+1 = "B" (nt == lead + 2); rb[0] is a
+  // row bit of A that B lacks, rb[1] a row bit of B that A lacks.  A lane
+  // computes the 4 rows over (rb[0], rb[1]) with 2 loads of A and 2 of B per
+  // summed value instead of 4 + 4.
+  uint8_t lead;
+  uint8_t rb[2];
 };
 static_assert(sizeof(DevOp) == 32, "DevOp layout");
 
@@ -50,13 +56,18 @@ struct alignas(16) DevTensor {
 };
 static_assert(sizeof(DevTensor) == 48, "DevTensor layout");
 
-// One level of the level-synchronous schedule: ops [op_begin, op_begin+op_count)
-// of the level-sorted op array, `items` warp work items in total.
+// One level of the level-synchronous schedule: generic ops
+// [op_begin, op_begin+op_count) of the level-sorted op array (`items` warp
+// work items), then its outer-join ops [op_begin+op_count, +outer_count)
+// (`outer_items` items, item_begin counted from 0 within that group).  The two
+// groups run as concurrent kernels.
 struct LevelLaunch {
   uint32_t op_begin;
   uint32_t op_count;
   uint32_t items;
-  uint32_t max_nt;  // widest member list in the level (selects the kernel instance)
+  uint32_t max_nt;  // widest member list of the generic ops (selects the kernel instance)
+  uint32_t outer_count;
+  uint32_t outer_items;
 };
 
 // Planner target for warp items per level: enough to cover every SM several

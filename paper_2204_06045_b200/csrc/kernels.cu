@@ -260,6 +260,126 @@ level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
   }
 }
 
+// Insert a zero bit at position q of x.
+__device__ __forceinline__ uint32_t insert_zero(uint32_t x, uint32_t q) {
+  return ((x >> q) << (q + 1)) | (x & ((1u << q) - 1u));
+}
+
+// Outer-join bucket (DevOp::lead/rb): out = sum_s  P_s * A_s * B_s with
+// P = the product of the `lead` row-invariant leading members.  The lane
+// computes the 4 rows over register bits (rb0: A-only, rb1: B-only) from 2+2
+// operand loads per summed value -- half the loads of the generic path --
+// while keeping the reference's left-fold order ((P*A)*B).
+template <int LEAD>
+__device__ __forceinline__ void run_outer(const DevOp& op, uint32_t chunk,
+                                          const DevTensor* __restrict__ trefs,
+                                          double2* __restrict__ arena, int lane, DevTensor* slot) {
+  constexpr int T = LEAD + 2;
+  const int cb = op.cb;  // >= 7 by construction
+  const uint64_t kbase = static_cast<uint64_t>(chunk) << cb;
+  const uint64_t khi = kbase | (static_cast<uint64_t>(lane) << 5);
+  const uint32_t r0 = op.rb[0], r1 = op.rb[1];
+  {
+    const uint4* src4 = reinterpret_cast<const uint4*>(trefs + op.tref);
+    uint4* dst4 = reinterpret_cast<uint4*>(slot);
+    if (lane < 3 * T) dst4[lane] = __ldg(src4 + lane);
+    __syncwarp();
+  }
+  const double2* base[T];
+  uint32_t lo[T], hi[T], sa[T], d0[T], d1[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const DevTensor& d = slot[t];
+    base[t] = arena + d.off;
+    const int rank = d.rank;
+    uint32_t l = 0, h = 0, a = 0, x0 = 0, x1 = 0;
+#pragma unroll 1
+    for (int ax = 0; ax < rank; ++ax) {
+      const uint32_t src = d.src[ax];
+      const uint32_t bit = 1u << (rank - 1 - ax);
+      if (src < 5) l |= ((static_cast<uint32_t>(lane) >> src) & 1u) ? bit : 0u;
+      else if (src == r0) x0 |= bit;
+      else if (src == r1) x1 |= bit;
+      else if (src < kSumSrc) h |= ((khi >> src) & 1u) ? bit : 0u;
+      else a |= bit;
+    }
+    lo[t] = l;
+    hi[t] = h;
+    sa[t] = a;
+    d0[t] = x0;
+    d1[t] = x1;
+  }
+  __syncwarp();
+  // prefix of the row-invariant leading members, both summed values
+  double2 pre0 = make_double2(1.0, 0.0), pre1 = pre0;
+#pragma unroll
+  for (int t = 0; t < LEAD; ++t) {
+    const double2* p = base[t] + lo[t] + __shfl_sync(kFull, hi[t], 0);
+    const double2 x = ld(p), y = ld(p + sa[t]);
+    pre0 = t == 0 ? x : cmul(pre0, x);
+    pre1 = t == 0 ? y : cmul(pre1, y);
+  }
+  const uint32_t q0 = r0 - 5u, q1 = r1 - 5u;
+  const uint32_t qa = q0 < q1 ? q0 : q1, qb = q0 < q1 ? q1 : q0;
+  const int steps = 1 << (cb - 7);
+  double2* out = arena + op.out + kbase + lane;
+  constexpr int A = LEAD, B = LEAD + 1;
+  for (int it = 0; it < steps; ++it) {
+    const uint32_t e = insert_zero(insert_zero(static_cast<uint32_t>(it), qa), qb);
+    const double2* pa = base[A] + lo[A] + __shfl_sync(kFull, hi[A], e);
+    const double2* pb = base[B] + lo[B] + __shfl_sync(kFull, hi[B], e);
+    const double2 a00 = ld(pa), a01 = ld(pa + sa[A]);                   // rb0 = 0
+    const double2 a10 = ld(pa + d0[A]), a11 = ld(pa + d0[A] + sa[A]);   // rb0 = 1
+    const double2 b00 = ld(pb), b01 = ld(pb + sa[B]);                   // rb1 = 0
+    const double2 b10 = ld(pb + d1[B]), b11 = ld(pb + d1[B] + sa[B]);   // rb1 = 1
+    const double2 p00 = LEAD ? cmul(pre0, a00) : a00, p01 = LEAD ? cmul(pre1, a01) : a01;
+    const double2 p10 = LEAD ? cmul(pre0, a10) : a10, p11 = LEAD ? cmul(pre1, a11) : a11;
+    const uint64_t r00 = static_cast<uint64_t>(e) << 5;
+    const uint64_t ra = static_cast<uint64_t>(1u << q0) << 5, rb = static_cast<uint64_t>(1u << q1) << 5;
+    out[r00] = cadd(cmul(p00, b00), cmul(p01, b01));
+    out[r00 + rb] = cadd(cmul(p00, b10), cmul(p01, b11));
+    out[r00 + ra] = cadd(cmul(p10, b00), cmul(p11, b01));
+    out[r00 + ra + rb] = cadd(cmul(p10, b10), cmul(p11, b11));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
+             const DevTensor* __restrict__ trefs, double2* __restrict__ arena,
+             uint32_t op_count, uint32_t items) {
+  __shared__ DevTensor slots[kWarpsPerCta][4];
+  __shared__ uint32_t sbeg[kSmemOps];
+  const bool cached = op_count <= kSmemOps;
+  if (cached)
+    for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  DevTensor* slot = slots[threadIdx.x >> 5];
+  const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+  uint32_t cur = 0, cur_begin = 1, cur_end = 0;
+  for (uint32_t item = warp; item < items; item += nwarps) {
+    if (item < cur_begin || item >= cur_end) {
+      uint32_t lo = 0, hi = op_count;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const uint32_t b = cached ? sbeg[mid] : __ldg(ibeg + mid);
+        if (b <= item) lo = mid; else hi = mid;
+      }
+      cur = lo;
+      cur_begin = cached ? sbeg[lo] : __ldg(ibeg + lo);
+      cur_end = lo + 1 < op_count ? (cached ? sbeg[lo + 1] : __ldg(ibeg + lo + 1)) : items;
+    }
+    const DevOp op = ops[cur];
+    const uint32_t chunk = item - cur_begin;
+    switch (op.lead) {
+      case 0: run_outer<0>(op, chunk, trefs, arena, lane, slot); break;
+      case 1: run_outer<1>(op, chunk, trefs, arena, lane, slot); break;
+      default: run_outer<2>(op, chunk, trefs, arena, lane, slot); break;
+    }
+  }
+}
+
 __global__ void final_kernel(const uint64_t* __restrict__ scalar_off,
                              const uint32_t* __restrict__ lc_begin, int n_lc,
                              const double2* __restrict__ arena, double2* __restrict__ terms) {
@@ -290,7 +410,30 @@ int grid_for(uint32_t items) {
   return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+int outer_grid(uint32_t items) {
+  static int cap = 0;
+  if (cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, outer_kernel, kThreads, 0);
+    cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const uint32_t want = (items + kWarpsPerCta - 1) / kWarpsPerCta;
+  return static_cast<int>(want < static_cast<uint32_t>(cap) ? (want > 0 ? want : 1) : cap);
+}
+
 }  // namespace
+
+cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
+                         const DevTensor* trefs, double2* arena, const LevelLaunch& lv) {
+  if (lv.outer_items == 0) return cudaSuccess;
+  const uint32_t first = lv.op_begin + lv.op_count;
+  outer_kernel<<<outer_grid(lv.outer_items), kThreads, 0, s>>>(ops + first, ibeg + first, trefs,
+                                                               arena, lv.outer_count,
+                                                               lv.outer_items);
+  return cudaGetLastError();
+}
 
 int level_grid(uint32_t items) { return grid_for<8>(items); }
 

@@ -15,6 +15,11 @@ int level_grid(uint32_t items);
 cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
                          const DevTensor* trefs, double2* arena, const LevelLaunch& lv);
 
+// The level's outer-join ops (DevOp::lead/rb), meant to run concurrently with
+// launch_level on a second stream.
+cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
+                         const DevTensor* trefs, double2* arena, const LevelLaunch& lv);
+
 // Resident warps of the level kernel on the current device.
 int resident_warps();
 
@@ -22,7 +27,10 @@ int resident_warps();
 cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint32_t* lc_begin,
                          int n_lc, const double2* arena, double2* terms);
 
-// Number of kernels launched per plan execution (levels + final).
-inline int kernels_per_plan(int n_levels) { return n_levels + 1; }
+// Number of kernels launched per plan execution (level kernels, outer-join
+// kernels, final).
+inline int kernels_per_plan(int n_level_launches, int n_outer_launches) {
+  return n_level_launches + n_outer_launches + 1;
+}
 
 }  // namespace qtng

@@ -5,6 +5,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "pool.hpp"
 
@@ -27,6 +28,15 @@ void mark_invariant_lead(DevOp& d, const DevTensor* ts) {
     if (src >= 5 && src < d.cb) return;
   }
   d.inv0 = 1;
+}
+
+// Tuning switch: QTNG_OUTER=0 routes outer-join ops through the generic kernel.
+bool outer_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("QTNG_OUTER");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 // Power-of-two size classes; a class's freed blocks are reused first-in
@@ -121,6 +131,54 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   }
   hp.arena_elems = arena.peak();
 
+  // item size per level: 32-output rows per warp item, fewer for small levels
+  // so the level still spreads over the whole GPU
+  std::vector<int> level_cb(n_levels);
+  for (int L = 0; L < n_levels; ++L) {
+    int row_bits = 0;
+    while (row_bits < kItemBits - 5 && (level_rows[L] >> (row_bits + 1)) >= kTargetItems) ++row_bits;
+    level_cb[L] = 5 + row_bits;
+  }
+  // outer-join classification (DevOp::lead/rb), in parallel
+  std::vector<uint32_t> outer_sig(N, 0);  // 0 = generic; else 1 | lead<<8 | rb0<<16 | rb1<<24
+  {
+    const int chunks = static_cast<int>(std::min<uint32_t>(N, 256));
+    Pool::get().parallel_for(chunks, [&](int ch) {
+      std::vector<uint8_t> pm(max_vars);
+      std::vector<uint32_t> pm_stamp(max_vars, ~0u);
+      for (uint32_t g = static_cast<uint32_t>(uint64_t{N} * ch / chunks);
+           g < static_cast<uint32_t>(uint64_t{N} * (ch + 1) / chunks); ++g) {
+        const Op& o = op_at(g);
+        const int cb = std::min<int>(o.r, level_cb[o.level]);
+        if (!outer_enabled() || o.ns != 1 || o.nin < 2 || o.nin > 4 || cb < 7) continue;
+        const WalkResult& w = *cones[lc_of[g]];
+        const int32_t* ov = w.out_vars(o);
+        for (int k = 0; k < o.r; ++k) { pm[ov[k]] = static_cast<uint8_t>(o.r - 1 - k); pm_stamp[ov[k]] = g; }
+        const uint64_t rowmask = ((uint64_t{1} << cb) - 1) & ~uint64_t{31};
+        uint64_t mask[kMaxInputs] = {};
+        const OpIn* ins = w.inputs(o);
+        for (int t = 0; t < o.nin; ++t)
+          for (int ax = 0; ax < ins[t].rank; ++ax) {
+            const int v = w.in_vars(ins[t])[ax];
+            if (pm_stamp[v] == g) mask[t] |= uint64_t{1} << pm[v];
+          }
+        int lead = 0;
+        while (lead < o.nin && (mask[lead] & rowmask) == 0) ++lead;
+        if (lead != o.nin - 2) continue;
+        const uint64_t a_only = mask[lead] & ~mask[lead + 1] & rowmask;
+        const uint64_t b_only = mask[lead + 1] & ~mask[lead] & rowmask;
+        if (!a_only || !b_only) continue;
+        const int rb0 = __builtin_ctzll(a_only), rb1 = __builtin_ctzll(b_only);
+        outer_sig[g] = 1u | (static_cast<uint32_t>(lead) << 8) | (static_cast<uint32_t>(rb0) << 16) |
+                       (static_cast<uint32_t>(rb1) << 24);
+      }
+    });
+  }
+  // generic ops first, outer-join ops last within each level (stable)
+  for (int L = 0; L < n_levels; ++L)
+    std::stable_partition(order.begin() + lstart[L], order.begin() + lstart[L + 1],
+                          [&](uint32_t g) { return outer_sig[g] == 0; });
+
   // descriptors, level by level: the item/tref prefix sums sequentially ...
   hp.ops.resize(N);
   hp.ibeg.resize(N);
@@ -129,25 +187,32 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   std::vector<double> op_bytes(N);
   uint32_t n_trefs = 0;
   for (int L = 0; L < n_levels; ++L) {
-    LevelLaunch ll{lstart[L], lstart[L + 1] - lstart[L], 0, 0};
-    // item size: 32-output rows per warp item, fewer for small levels so the
-    // level still spreads over the whole GPU
-    int row_bits = 0;
-    while (row_bits < kItemBits - 5 && (level_rows[L] >> (row_bits + 1)) >= kTargetItems) ++row_bits;
+    LevelLaunch ll{lstart[L], 0, 0, 0, 0, 0};
     for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) {
-      const Op& o = op_at(order[i]);
+      const uint32_t g = order[i];
+      const Op& o = op_at(g);
+      const bool outer = outer_sig[g] != 0;
       DevOp& d = hp.ops[i];
-      d.out = out[order[i]];
-      d.item_begin = ll.items;
+      d.out = out[g];
       d.tref = n_trefs;
       d.r = static_cast<uint8_t>(o.r);
       d.ns = static_cast<uint8_t>(o.ns);
       d.nt = static_cast<uint8_t>(o.nin);
-      d.cb = static_cast<uint8_t>(std::min<int>(o.r, 5 + row_bits));
-      ll.max_nt = std::max<uint32_t>(ll.max_nt, d.nt);
+      d.cb = static_cast<uint8_t>(std::min<int>(o.r, level_cb[L]));
+      d.lead = outer ? static_cast<uint8_t>((outer_sig[g] >> 8) & 0xff) : 0;
+      d.rb[0] = outer ? static_cast<uint8_t>((outer_sig[g] >> 16) & 0xff) : 0;
+      d.rb[1] = outer ? static_cast<uint8_t>(outer_sig[g] >> 24) : 0;
+      uint32_t& items_acc = outer ? ll.outer_items : ll.items;
+      d.item_begin = items_acc;
       const uint64_t items = uint64_t{1} << (o.r - d.cb);
-      if (ll.items + items > 0xffffffffull) throw Error(kResource, "level has too many work items");
-      ll.items += static_cast<uint32_t>(items);
+      if (items_acc + items > 0xffffffffull) throw Error(kResource, "level has too many work items");
+      items_acc += static_cast<uint32_t>(items);
+      if (outer) {
+        ++ll.outer_count;
+      } else {
+        ++ll.op_count;
+        ll.max_nt = std::max<uint32_t>(ll.max_nt, d.nt);
+      }
       hp.ibeg[i] = d.item_begin;
       hp.op_width[i] = o.bucket_seq >= 0 ? o.width : 0;
       n_trefs += static_cast<uint32_t>(o.nin);
