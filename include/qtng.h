@@ -75,6 +75,10 @@ typedef struct qtng_plan_info {
   uint64_t arena_bytes;      /* peak HBM arena footprint */
   uint64_t desc_bytes;       /* descriptor bytes uploaded per plan */
   int32_t kernels_per_run;   /* kernel launches per execution */
+  uint64_t n_segments;       /* fused-chain segments (seg_kernel units) */
+  uint64_t n_fused_ops;      /* bucket ops evaluated inside segments */
+  double dev_bytes;          /* HBM bytes the fused program must move: per
+                                unit, its materialised inputs + its output */
 } qtng_plan_info;
 
 /* ---------------------------------------------------------------- context */
@@ -188,6 +192,10 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
  * throughput measurement; n_runs back-to-back runs, total device time. */
 qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms);
 qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info);
+/* Host-only: the plan qtng_plan_create would build for all m edges (fuse=1:
+ * fused-chain segments, fuse=0: one device op per bucket), without a device. */
+qtng_status qtng_plan_stats(int n, int m, const int* edges, int p, int merged,
+                            int max_result_width, int fuse, qtng_plan_info* info);
 /* Records of the last execution (edge_u/edge_v filled from the selection). */
 qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64_t cap,
                               int64_t* n_out);

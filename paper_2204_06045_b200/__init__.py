@@ -406,6 +406,17 @@ def plan_dump(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfig
     return out
 
 
+def plan_stats(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfig] = None,
+               fuse: bool = True) -> PlanInfo:
+    """Host-only: the PlanInfo Plan(g, p) would have (fuse=False: one device
+    op per bucket, no fused-chain segments)."""
+    cfg = cfg or EngineConfig()
+    inf = PlanInfo()
+    _check(lib.qtng_plan_stats(g.n, g.m, g.flat(), p, int(merged), cfg.max_result_width,
+                               int(fuse), C.byref(inf)))
+    return inf
+
+
 def validate_energy(g: Graph, p: int, merged: bool = False,
                     cfg: Optional[EngineConfig] = None) -> None:
     """Host-only pre-flight of energy_expectation: raises the ScheduleError

@@ -33,7 +33,8 @@ class PlanInfo(C.Structure):
                 ("max_width", C.c_int32), ("max_result_rank", C.c_int32),
                 ("alg_bytes", C.c_double), ("sum_ops", C.c_double),
                 ("arena_bytes", C.c_uint64), ("desc_bytes", C.c_uint64),
-                ("kernels_per_run", C.c_int32)]
+                ("kernels_per_run", C.c_int32), ("n_segments", C.c_uint64),
+                ("n_fused_ops", C.c_uint64), ("dev_bytes", C.c_double)]
 
 
 def _load():
@@ -75,6 +76,8 @@ def _load():
                                       C.POINTER(C.c_float)]
     lib.qtng_plan_run_device.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
     lib.qtng_plan_info_get.argtypes = [vp, C.POINTER(PlanInfo)]
+    lib.qtng_plan_stats.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(PlanInfo)]
     lib.qtng_plan_records.argtypes = [vp, C.POINTER(Record), C.c_int64, C.POINTER(C.c_int64)]
     lib.qtng_plan_level_ms.argtypes = [vp, f32p, C.c_int]
     lib.qtng_plan_destroy.argtypes = [vp]
@@ -91,6 +94,6 @@ EXPORTED = [
     "qtng_create", "qtng_destroy", "qtng_last_error", "qtng_version", "qtng_random_regular",
     "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
     "qtng_contract_schedule", "qtng_energy", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute",
-    "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_records", "qtng_plan_level_ms",
+    "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_plan_records", "qtng_plan_level_ms",
     "qtng_plan_destroy", "qtng_plan_time_level",
 ]

@@ -151,7 +151,8 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
 
 // Descriptor image of a HostPlan: one contiguous blob, 256-byte aligned sections.
 struct DescLayout {
-  size_t ops = 0, ibeg = 0, trefs = 0, scal = 0, lcb = 0, terms = 0, total = 0;
+  size_t ops = 0, ibeg = 0, trefs = 0, segs = 0, seg_ibeg = 0, stages = 0, ctr = 0, scal = 0,
+         lcb = 0, terms = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t{255}; }
@@ -162,6 +163,10 @@ DescLayout layout_of(const HostPlan& hp) {
   L.ops = o; o = align256(o + hp.ops.size() * sizeof(DevOp));
   L.ibeg = o; o = align256(o + hp.ibeg.size() * sizeof(uint32_t));
   L.trefs = o; o = align256(o + hp.trefs.size() * sizeof(DevTensor));
+  L.segs = o; o = align256(o + hp.segs.size() * sizeof(DevSeg));
+  L.seg_ibeg = o; o = align256(o + hp.seg_ibeg.size() * sizeof(uint32_t));
+  L.stages = o; o = align256(o + hp.stages.size() * sizeof(DevStage));
+  L.ctr = o; o = align256(o + hp.levels.size() * 2 * sizeof(uint32_t));
   L.scal = o; o = align256(o + hp.scalar_off.size() * sizeof(uint64_t));
   L.lcb = o; o = align256(o + hp.lc_begin.size() * sizeof(uint32_t));
   L.terms = o; o = align256(o + (hp.lc_begin.size()) * sizeof(double2));
@@ -173,6 +178,10 @@ void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
   std::memcpy(dst + L.ops, hp.ops.data(), hp.ops.size() * sizeof(DevOp));
   std::memcpy(dst + L.ibeg, hp.ibeg.data(), hp.ibeg.size() * sizeof(uint32_t));
   std::memcpy(dst + L.trefs, hp.trefs.data(), hp.trefs.size() * sizeof(DevTensor));
+  std::memcpy(dst + L.segs, hp.segs.data(), hp.segs.size() * sizeof(DevSeg));
+  std::memcpy(dst + L.seg_ibeg, hp.seg_ibeg.data(), hp.seg_ibeg.size() * sizeof(uint32_t));
+  std::memcpy(dst + L.stages, hp.stages.data(), hp.stages.size() * sizeof(DevStage));
+  std::memset(dst + L.ctr, 0, hp.levels.size() * 2 * sizeof(uint32_t));  // seg_kernel work counters
   std::memcpy(dst + L.scal, hp.scalar_off.data(), hp.scalar_off.size() * sizeof(uint64_t));
   std::memcpy(dst + L.lcb, hp.lc_begin.data(), hp.lc_begin.size() * sizeof(uint32_t));
 }
@@ -190,7 +199,8 @@ struct qtng_ctx {
   DevBuf desc;           // scratch descriptors (one-shot calls)
   PinBuf pin_desc, pin_in, pin_out;
   cudaStream_t stream2 = nullptr;  // outer-join kernels, forked per level
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t stream3 = nullptr;  // fused-chain segment kernels, forked per level
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, join3_ev = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   void ensure_arena(uint64_t elems) {
@@ -216,23 +226,39 @@ struct DevProgram {
   const DevOp* ops() const { return reinterpret_cast<const DevOp*>(base + L.ops); }
   const uint32_t* ibeg() const { return reinterpret_cast<const uint32_t*>(base + L.ibeg); }
   const DevTensor* trefs() const { return reinterpret_cast<const DevTensor*>(base + L.trefs); }
+  const DevSeg* segs() const { return reinterpret_cast<const DevSeg*>(base + L.segs); }
+  const uint32_t* seg_ibeg() const { return reinterpret_cast<const uint32_t*>(base + L.seg_ibeg); }
+  const DevStage* stages() const { return reinterpret_cast<const DevStage*>(base + L.stages); }
+  uint32_t* ctr(size_t level) const { return reinterpret_cast<uint32_t*>(base + L.ctr) + 2 * level; }
   const uint64_t* scal() const { return reinterpret_cast<const uint64_t*>(base + L.scal); }
   const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
   double2* terms() const { return reinterpret_cast<double2*>(base + L.terms); }
 };
 
-// One level: the outer-join kernel forked onto the side stream, the generic
-// kernel on the main stream, joined before the next level.
-void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, const DevProgram& pr, double2* arena) {
-  const bool fork = lv.outer_items > 0;
-  if (fork) {
-    QTNG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+// One level: the outer-join and segment kernels forked onto side streams, the
+// generic kernel on the main stream, joined before the next level.
+void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const DevProgram& pr,
+                   double2* arena) {
+  const bool fork2 = lv.outer_items > 0;
+  const bool fork3 = lv.seg_items > 0 && (lv.items > 0 || fork2);
+  if (fork2 || fork3) QTNG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+  if (fork2) {
     QTNG_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->fork_ev, 0));
     QTNG_CUDA(launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
     QTNG_CUDA(cudaEventRecord(ctx->join_ev, ctx->stream2));
   }
+  if (fork3) {
+    QTNG_CUDA(cudaStreamWaitEvent(ctx->stream3, ctx->fork_ev, 0));
+    QTNG_CUDA(launch_segs(ctx->stream3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(), arena,
+                          pr.ctr(level), lv));
+    QTNG_CUDA(cudaEventRecord(ctx->join3_ev, ctx->stream3));
+  } else {
+    QTNG_CUDA(launch_segs(ctx->stream, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(), arena,
+                          pr.ctr(level), lv));
+  }
   QTNG_CUDA(launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
-  if (fork) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+  if (fork2) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+  if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join3_ev, 0));
 }
 
 // Enqueue the whole program on the context's stream: every level, then the
@@ -242,7 +268,7 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, do
   cudaStream_t s = ctx->stream;
   for (size_t L = 0; L < hp.levels.size(); ++L) {
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
-    enqueue_level(ctx, hp.levels[L], pr, arena);
+    enqueue_level(ctx, hp.levels[L], L, pr, arena);
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
   QTNG_CUDA(launch_final(s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
@@ -250,12 +276,13 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, do
 }
 
 int launches_per_run(const HostPlan& hp) {
-  int lv = 0, outer = 0;
+  int lv = 0, outer = 0, seg = 0;
   for (const LevelLaunch& l : hp.levels) {
     lv += l.items > 0;
     outer += l.outer_items > 0;
+    seg += l.seg_items > 0;
   }
-  return kernels_per_plan(lv, outer);
+  return kernels_per_plan(lv, outer, seg);
 }
 
 // Ops of the reference's run_edge post-processing (engine.cpp:517-519, 543-546).
@@ -305,10 +332,12 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
     QTNG_CUDA(cudaSetDevice(device));
     QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->stream3, cudaStreamNonBlocking));
     QTNG_CUDA(cudaEventCreate(&ctx->ev0));
     QTNG_CUDA(cudaEventCreate(&ctx->ev1));
     QTNG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
     QTNG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+    QTNG_CUDA(cudaEventCreateWithFlags(&ctx->join3_ev, cudaEventDisableTiming));
     if (arena_bytes) ctx->ensure_arena(arena_bytes / sizeof(double2));
     *out = ctx.release();
   });
@@ -319,12 +348,14 @@ void qtng_destroy(qtng_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->stream2);
-  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev})
+  cudaStreamSynchronize(ctx->stream3);
+  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev})
     if (e) cudaEventDestroy(e);
-  cudaStream_t s = ctx->stream, s2 = ctx->stream2;
+  cudaStream_t s = ctx->stream, s2 = ctx->stream2, s3 = ctx->stream3;
   delete ctx;  // frees the arena and staging buffers
   if (s) cudaStreamDestroy(s);
   if (s2) cudaStreamDestroy(s2);
+  if (s3) cudaStreamDestroy(s3);
 }
 
 qtng_status qtng_random_regular(int n, int d, uint64_t seed, int* edges, int cap, int* m_out) {
@@ -421,7 +452,8 @@ qtng_status qtng_plan_dump(int n, int m, const int* edges, int p, int merged,
       if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
       ptrs.push_back(&w);
     }
-    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems);
+    // every op as its own device op (no chain fusion): the op-class view
+    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, false);
     std::vector<int> out;
     for (size_t L = 0; L < hp.levels.size(); ++L)
       for (uint32_t k = 0; k < hp.levels[L].op_count + hp.levels[L].outer_count; ++k) {
@@ -705,11 +737,9 @@ qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms) 
   });
 }
 
-qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info) {
-  return guarded([&] {
-    if (!plan || !info) throw Error(kInvalidInput, "null argument");
-    const HostPlan& hp = plan->hp;
-    info->n_lightcones = static_cast<int32_t>(plan->edges.size());
+namespace {
+void fill_info(const HostPlan& hp, int n_lightcones, qtng_plan_info* info) {
+    info->n_lightcones = n_lightcones;
     info->n_levels = static_cast<int32_t>(hp.levels.size());
     info->n_buckets = hp.n_buckets;
     info->n_device_ops = hp.ops.size();
@@ -718,8 +748,38 @@ qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info) {
     info->alg_bytes = hp.alg_bytes;
     info->sum_ops = hp.sum_ops;
     info->arena_bytes = hp.arena_elems * sizeof(double2);
-    info->desc_bytes = plan->prog.L.total;
+    info->desc_bytes = layout_of(hp).total;
     info->kernels_per_run = launches_per_run(hp);
+    info->n_segments = hp.segs.size();
+    info->n_fused_ops = hp.n_fused_ops;
+    info->dev_bytes = hp.dev_bytes;
+}
+}  // namespace
+
+qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info) {
+  return guarded([&] {
+    if (!plan || !info) throw Error(kInvalidInput, "null argument");
+    fill_info(plan->hp, static_cast<int>(plan->edges.size()), info);
+  });
+}
+
+qtng_status qtng_plan_stats(int n, int m, const int* edges, int p, int merged,
+                            int max_result_width, int fuse, qtng_plan_info* info) {
+  return guarded([&] {
+    if (!info) throw Error(kInvalidInput, "null argument");
+    if (p < 1) throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+    const Graph g = graph_from(n, m, edges);
+    const ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, selection(m, m, nullptr));
+    std::vector<const WalkResult*> ptrs;
+    for (size_t i = 0; i < cs.walks.size(); ++i) {
+      if (cs.walks[i].fail_code)
+        throw Error(kSchedule, "edge (" + std::to_string(cs.edges[i].u) + ", " +
+                                   std::to_string(cs.edges[i].v) + "): " + cs.walks[i].fail_msg);
+      ptrs.push_back(&cs.walks[i]);
+    }
+    const HostPlan hp =
+        build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse != 0);
+    fill_info(hp, static_cast<int>(ptrs.size()), info);
   });
 }
 
@@ -777,9 +837,9 @@ qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* le
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     ctx->ensure_arena(hp.arena_elems);
-    enqueue_level(ctx, hp.levels[level], plan->prog, ctx->A());  // warm-up
+    enqueue_level(ctx, hp.levels[level], level, plan->prog, ctx->A());  // warm-up
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    for (int i = 0; i < n_runs; ++i) enqueue_level(ctx, hp.levels[level], plan->prog, ctx->A());
+    for (int i = 0; i < n_runs; ++i) enqueue_level(ctx, hp.levels[level], level, plan->prog, ctx->A());
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;

@@ -56,6 +56,52 @@ struct alignas(16) DevTensor {
 };
 static_assert(sizeof(DevTensor) == 48, "DevTensor layout");
 
+// ---------------------------------------------------------------- fused chains
+// A segment is a chain of L >= 2 bucket contractions op_1 -> ... -> op_L in
+// which op_i (i >= 2) consumes op_{i-1}'s result as its LAST member (the
+// "main") and that result spans op_i's whole width (every var of op_i), so
+// each element of the intermediate X_{i-1} is used exactly once.  Only
+// Y = X_L reaches HBM; the seg_kernel keeps X_1 .. X_{L-1} in registers.
+//
+// Index space.  A warp tile fixes Y's high rY-cY bits (the tile number) and
+// its lanes cover Y's low cY = min(rY, 5) bits.  Each lane walks the
+// J = L-1 digits j: bit i-2 of j is s_i, the var summed by stage i >= 2.
+// DevTensor::src codes of a segment operand:
+//   0..4     lane bit (Y bit b < cY)
+//   8..15    digit bit (code - 8 = i - 2 for s_i)
+//   32..63   tile-number bit (code - 32 = Y bit - cY)
+//   64       stage 1's own summed bit (stage 1 sums at most one var)
+constexpr int kSegYBits = 5;         // cY = min(rY, kSegYBits)
+constexpr int kSegMaxJ = 8;          // digits per segment (dlo/dhi tables: 2 x 4 bits)
+constexpr int kSegMaxStages = kSegMaxJ + 1;
+constexpr int kSegMaxOps = 16;       // operands per segment (all stages)
+constexpr int kSegMaxNt1 = 6;        // members of stage 1
+constexpr int kSegMaxNt = 4;         // members of a fused stage (incl. the main)
+constexpr uint8_t kSegMain = 0xff;   // DevStage::main of stage 1 (no main)
+constexpr uint8_t kLaneSrcEnd = 5;
+constexpr uint8_t kJSrc = 8;
+constexpr uint8_t kTileSrc = 32;
+
+struct alignas(16) DevSeg {
+  uint64_t out;         // arena element offset of Y
+  uint32_t item_begin;  // first tile of this segment inside its level's segment group
+  uint32_t tref;        // first DevTensor (stage 1's members, then stage 2's, ...)
+  uint32_t stage;       // first DevStage
+  uint8_t nst;          // L
+  uint8_t ry;           // rank of Y
+  uint8_t cy;           // in-tile Y bits
+  uint8_t nops;         // DevTensors of the segment (mains included as placeholders)
+};
+static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
+
+struct DevStage {
+  uint8_t nt;    // members (bucket member order)
+  uint8_t main;  // position of the main member (kSegMain for stage 1)
+  uint8_t ns;    // summed bits of the stage (0 or 1)
+  uint8_t op0;   // index of member 0 among the segment's DevTensors
+};
+static_assert(sizeof(DevStage) == 4, "DevStage layout");
+
 // One level of the level-synchronous schedule: generic ops
 // [op_begin, op_begin+op_count) of the level-sorted op array (`items` warp
 // work items), then its outer-join ops [op_begin+op_count, +outer_count)
@@ -68,6 +114,9 @@ struct LevelLaunch {
   uint32_t max_nt;  // widest member list of the generic ops (selects the kernel instance)
   uint32_t outer_count;
   uint32_t outer_items;
+  uint32_t seg_begin;  // fused-chain segments [seg_begin, seg_begin+seg_count)
+  uint32_t seg_count;
+  uint32_t seg_items;  // tiles
 };
 
 // Planner target for warp items per level: enough to cover every SM several

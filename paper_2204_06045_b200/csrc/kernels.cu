@@ -380,6 +380,248 @@ outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
   }
 }
 
+// ---------------------------------------------------------------- fused chains
+// seg_kernel: one warp evaluates one tile of a segment (device_plan.hpp):
+// lane l owns Y output (tile << cY) + l and walks the 2^J digit assignments j
+// (digit s_2 fastest) in post order.  For every j it evaluates stage 1 from
+// HBM/L1 into a register, then climbs the chain: stage i's term
+// P_i(s_i) * X_{i-1}(s_i) (P_i = left fold of its side members, s_i = bit
+// i-2 of j) is parked in acc[i] when s_i = 0 and completes X_i = acc[i] +
+// term when s_i = 1, which then feeds stage i+1.  No intermediate leaves the
+// register file, no barrier is needed, and every X_i element is produced by
+// the unfused bucket's exact operation sequence (left-fold product in member
+// order, ascending summed values), so results are bit-identical.
+struct ChainWarp {
+  uint64_t off[kSegMaxOps];              // arena offset of each operand
+  uint32_t llane[kSegMaxOps][32];        // lane part of the operand offset
+  uint32_t base[kSegMaxOps][32];         // lane + current tile part
+  uint32_t dtile[kSegMaxOps][32];        // delta per tile-number bit
+  uint32_t dj[kSegMaxOps][kSegMaxJ];     // delta per j bit
+  uint32_t inc[kSegMaxOps][kSegMaxJ];    // stage 1: offset step when j increments past bit b
+  uint32_t dlo[kSegMaxOps][16];          // offset of j bits 0..3
+  uint32_t dhi[kSegMaxOps][16];          // offset of j bits 4..7
+  uint32_t sd[kSegMaxOps];               // stage 1: offset of its summed bit
+  DevStage st[kSegMaxStages];
+  double2 acc[kSegMaxStages - 3][32];    // per lane: parked s_i = 0 terms of stages >= 4
+};
+
+// Per-segment operand tables (one warp).
+__device__ void chain_decode(ChainWarp& cw, const DevSeg& sg, const DevStage* __restrict__ stages,
+                             const DevTensor* __restrict__ trefs, int lane) {
+  __syncwarp();
+  if (lane < sg.nst) cw.st[lane] = stages[sg.stage + lane];
+  for (int op = 0; op < sg.nops; ++op) {
+    const DevTensor* d = trefs + sg.tref + op;
+    const int rank = d->rank;
+    uint32_t lv = 0, dt = 0, s = 0, dj = 0;  // lane: own part; lane b: tile bit b / j bit b delta
+    for (int ax = 0; ax < rank; ++ax) {
+      const uint32_t code = __ldg(&d->src[ax]);
+      const uint32_t bit = 1u << (rank - 1 - ax);
+      if (code < kLaneSrcEnd) lv |= ((lane >> code) & 1u) ? bit : 0u;
+      else if (code < kTileSrc) dj |= (code - kJSrc == static_cast<uint32_t>(lane)) ? bit : 0u;
+      else if (code < kSumSrc) dt |= (code - kTileSrc == static_cast<uint32_t>(lane)) ? bit : 0u;
+      else s = bit;
+    }
+    cw.llane[op][lane] = lv;
+    cw.dtile[op][lane] = dt;
+    if (lane < kSegMaxJ) cw.dj[op][lane] = dj;
+    // inc[b] = dj[b] - sum_{b' < b} dj[b'];  dlo/dhi: subset sums of j bits 0..3 / 4..7
+    uint32_t below = 0;
+    for (int b = 0; b < kSegMaxJ; ++b) {
+      const uint32_t djb = __shfl_sync(kFull, dj, b);
+      if (lane == b) cw.inc[op][b] = djb - below;
+      below += djb;
+    }
+    uint32_t lo = 0, hi = 0;
+    for (int b = 0; b < 4; ++b) {  // every lane takes part in the shuffles
+      const uint32_t xl = __shfl_sync(kFull, dj, b), xh = __shfl_sync(kFull, dj, b + 4);
+      lo += ((lane >> b) & 1) ? xl : 0u;
+      hi += ((lane >> b) & 1) ? xh : 0u;
+    }
+    if (lane < 16) {
+      cw.dlo[op][lane] = lo;
+      cw.dhi[op][lane] = hi;
+    }
+    if (lane == 0) {
+      cw.sd[op] = s;
+      cw.off[op] = d->off;
+    }
+  }
+  __syncwarp();
+}
+
+// Side-member product P_i (left fold of members [op0, op0+m)) at digit
+// assignment j; m >= 1.
+__device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const double2* __restrict__ arena,
+                                              int op0, int m, uint32_t j, int lane) {
+  const uint32_t jl = j & 15u, jh = j >> 4;
+  double2 p = make_double2(0.0, 0.0);
+  for (int t = 0; t < m; ++t) {
+    const int op = op0 + t;
+    const double2 x = ld(arena + cw.off[op] + (cw.base[op][lane] + cw.dlo[op][jl] + cw.dhi[op][jh]));
+    p = t == 0 ? x : cmul(p, x);
+  }
+  return p;
+}
+
+// term of stage i (DevStage st) at digit assignment j: P_i(j) * v, or v.
+__device__ __forceinline__ double2 chain_term(const ChainWarp& cw, const double2* __restrict__ arena,
+                                              const DevStage st, uint32_t j, double2 v, int lane) {
+  const int m = st.nt - 1;
+  return m ? cmul(chain_side(cw, arena, st.op0, m, j, lane), v) : v;
+}
+
+// One tile: 2^J stage-1 evaluations (NT members, NS summed bits), in groups
+// of 2^U consecutive j (stages 2..U+1 resolved in registers, four independent
+// stage-1 products in flight), then the climb above each group.
+template <int NT, int NS, int U>
+__device__ __forceinline__ void chain_tile(ChainWarp& cw, const DevSeg& sg,
+                                           double2* __restrict__ arena, uint32_t tile, int lane) {
+  constexpr int G = 1 << U;
+  const int L = sg.nst;
+  const uint32_t nj = 1u << (L - 1);
+  const double2* B[NT];
+  uint32_t o[NT], sdl[NT], d0[NT], d1[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    B[t] = arena + cw.off[t];
+    o[t] = cw.base[t][lane];
+    sdl[t] = cw.sd[t];
+    d0[t] = cw.dj[t][0];
+    d1[t] = U > 1 ? cw.dj[t][1] : 0u;
+  }
+  const DevStage st2 = cw.st[1];
+  const DevStage st3 = U > 1 ? cw.st[2] : st2;
+  for (uint32_t j = 0; j < nj; j += G) {
+    if (j) {  // from j - G (low U bits clear) to j: inc[b] assumes bits < b were set
+      const int b = __ffs(j) - 1;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) o[t] += cw.inc[t][b] + d0[t] + d1[t];
+    }
+    double2 v[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      uint32_t oq[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) oq[t] = o[t] + ((q & 1) ? d0[t] : 0u) + ((q & 2) ? d1[t] : 0u);
+      double2 x = ld(B[0] + oq[0]);
+#pragma unroll
+      for (int t = 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
+      if (NS) {
+        double2 p = ld(B[0] + oq[0] + sdl[0]);
+#pragma unroll
+        for (int t = 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
+        x = cadd(x, p);
+      }
+      v[q] = x;
+    }
+    // stage 2 over bit 0, stage 3 over bit 1 (U == 2)
+    double2 x = cadd(chain_term(cw, arena, st2, j, v[0], lane), chain_term(cw, arena, st2, j | 1u, v[1], lane));
+    if (U > 1) {
+      const double2 y = cadd(chain_term(cw, arena, st2, j | 2u, v[2], lane),
+                             chain_term(cw, arena, st2, j | 3u, v[3], lane));
+      x = cadd(chain_term(cw, arena, st3, j, x, lane), chain_term(cw, arena, st3, j | 2u, y, lane));
+    }
+    // climb: stage i = k + 2 >= U + 2 while the carry propagates
+    const uint32_t jj = j | (G - 1);
+    bool carry = true;
+    for (int k = U; k + 2 <= L; ++k) {
+      const double2 term = chain_term(cw, arena, cw.st[k + 1], jj, x, lane);
+      if (!((jj >> k) & 1u)) {
+        cw.acc[k - 2][lane] = term;
+        carry = false;
+        break;
+      }
+      x = cadd(cw.acc[k - 2][lane], term);
+    }
+    if (carry && lane < (1 << sg.cy)) arena[sg.out + (static_cast<uint64_t>(tile) << sg.cy) + lane] = x;
+  }
+}
+
+template <int NT, int NS>
+__device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const DevSeg& sg, double2* __restrict__ arena,
+                                             uint32_t tile, int lane) {
+  if (sg.nst >= 3) chain_tile<NT, NS, 2>(cw, sg, arena, tile, lane);
+  else chain_tile<NT, NS, 1>(cw, sg, arena, tile, lane);
+}
+
+#ifndef QTNG_SEG_MINB
+#define QTNG_SEG_MINB 20  // resident one-warp CTAs per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(32, QTNG_SEG_MINB)
+seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
+           const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
+           double2* __restrict__ arena, uint32_t seg_count, uint32_t items, uint32_t* ctr) {
+  __shared__ ChainWarp cw;
+  const int lane = threadIdx.x;
+  // dynamic tile queue (segments are sorted by per-tile cost, largest first);
+  // ctr[0] = next tile, ctr[1] = finished warps; the last warp resets both
+  int cur = -1;
+  uint32_t cur_begin = 0, cur_end = 0;
+  DevSeg sg{};
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(ctr, 1u);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= items) break;
+    if (cur < 0 || item < cur_begin || item >= cur_end) {
+      uint32_t lo = 0, hi = seg_count;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ibeg + mid) <= item) lo = mid; else hi = mid;
+      }
+      if (static_cast<int>(lo) != cur) {
+        cur = static_cast<int>(lo);
+        sg = segs[lo];
+        chain_decode(cw, sg, stages, trefs, lane);
+      }
+      cur_begin = __ldg(ibeg + lo);
+      cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
+    }
+    const uint32_t tile = item - cur_begin;
+    for (int op = 0; op < sg.nops; ++op) {
+      const uint32_t v = ((tile >> lane) & 1u) ? cw.dtile[op][lane] : 0u;
+      cw.base[op][lane] = cw.llane[op][lane] + __reduce_add_sync(kFull, v);
+    }
+    __syncwarp();
+    const DevStage s1 = cw.st[0];
+    switch (s1.nt * 2 + s1.ns) {
+      case 2: chain_tile_u<1, 0>(cw, sg, arena, tile, lane); break;
+      case 3: chain_tile_u<1, 1>(cw, sg, arena, tile, lane); break;
+      case 4: chain_tile_u<2, 0>(cw, sg, arena, tile, lane); break;
+      case 5: chain_tile_u<2, 1>(cw, sg, arena, tile, lane); break;
+      case 6: chain_tile_u<3, 0>(cw, sg, arena, tile, lane); break;
+      case 7: chain_tile_u<3, 1>(cw, sg, arena, tile, lane); break;
+      case 8: chain_tile_u<4, 0>(cw, sg, arena, tile, lane); break;
+      case 9: chain_tile_u<4, 1>(cw, sg, arena, tile, lane); break;
+      case 10: chain_tile_u<5, 0>(cw, sg, arena, tile, lane); break;
+      case 11: chain_tile_u<5, 1>(cw, sg, arena, tile, lane); break;
+      case 12: chain_tile_u<6, 0>(cw, sg, arena, tile, lane); break;
+      default: chain_tile_u<6, 1>(cw, sg, arena, tile, lane); break;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every warp has left the queue
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
+int seg_grid(uint32_t items) {
+  static int cap = 0;
+  if (cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_kernel, 32, 0);
+    cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return static_cast<int>(items < static_cast<uint32_t>(cap) ? (items > 0 ? items : 1) : cap);
+}
+
 __global__ void final_kernel(const uint64_t* __restrict__ scalar_off,
                              const uint32_t* __restrict__ lc_begin, int n_lc,
                              const double2* __restrict__ arena, double2* __restrict__ terms) {
@@ -432,6 +674,16 @@ cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
   outer_kernel<<<outer_grid(lv.outer_items), kThreads, 0, s>>>(ops + first, ibeg + first, trefs,
                                                                arena, lv.outer_count,
                                                                lv.outer_items);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
+                        const DevStage* stages, const DevTensor* trefs, double2* arena,
+                        uint32_t* ctr, const LevelLaunch& lv) {
+  if (lv.seg_items == 0) return cudaSuccess;
+  seg_kernel<<<seg_grid(lv.seg_items), 32, 0, s>>>(
+      segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, trefs, arena, lv.seg_count,
+      lv.seg_items, ctr);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,11 @@ cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
 cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
                          const DevTensor* trefs, double2* arena, const LevelLaunch& lv);
 
+// The level's fused-chain segments (seg_kernel), concurrent with the others.
+cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
+                        const DevStage* stages, const DevTensor* trefs, double2* arena,
+                        uint32_t* ctr, const LevelLaunch& lv);
+
 // Resident warps of the level kernel on the current device.
 int resident_warps();
 
@@ -28,9 +33,9 @@ cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint3
                          int n_lc, const double2* arena, double2* terms);
 
 // Number of kernels launched per plan execution (level kernels, outer-join
-// kernels, final).
-inline int kernels_per_plan(int n_level_launches, int n_outer_launches) {
-  return n_level_launches + n_outer_launches + 1;
+// kernels, segment kernels, final).
+inline int kernels_per_plan(int n_level_launches, int n_outer_launches, int n_seg_launches) {
+  return n_level_launches + n_outer_launches + n_seg_launches + 1;
 }
 
 }  // namespace qtng

@@ -68,7 +68,25 @@ class ClassArena {
 
 }  // namespace
 
-HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems) {
+// Digits per segment (L - 1): QTNG_SEG_J, default kSegMaxJ.
+int seg_max_j() {
+  static const int j = [] {
+    const char* v = std::getenv("QTNG_SEG_J");
+    const int x = v ? std::atoi(v) : kSegMaxJ;
+    return std::max(1, std::min(x, kSegMaxJ));
+  }();
+  return j;
+}
+
+bool fuse_default() {
+  static const bool on = [] {
+    const char* v = std::getenv("QTNG_FUSE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems, bool fuse) {
   HostPlan hp;
   hp.input_elems = input_elems;
   const int C = static_cast<int>(cones.size());
@@ -81,7 +99,6 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   }
   const uint32_t N = base[C];
   std::vector<uint32_t> lc_of(N);
-  int max_level = -1;
   for (int c = 0; c < C; ++c)
     for (uint32_t k = 0; k < cones[c]->ops.size(); ++k) {
       const Op& o = cones[c]->ops[k];
@@ -91,20 +108,92 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
                                        " variables; the device path supports at most " +
                                        std::to_string(kMaxSumBits));
       lc_of[base[c] + k] = c;
-      max_level = std::max(max_level, static_cast<int>(o.level));
     }
-  const int n_levels = max_level + 1;
   auto op_at = [&](uint32_t g) -> const Op& { return cones[lc_of[g]]->ops[g - base[lc_of[g]]]; };
 
-  // stable counting sort by level; release lists by consumer level
-  std::vector<uint32_t> lstart(n_levels + 1, 0), order(N);
+  // ---- units: single ops, or fused chains (segments, see device_plan.hpp)
+  // main_pos[g]: position of op g's fused main member, -1 when g heads its unit
+  std::vector<int8_t> main_pos(N, -1);
+  std::vector<uint32_t> unit_of(N);
+  std::vector<uint32_t> unit_first, unit_last, unit_len, unit_nops;  // per unit
+  std::vector<uint32_t> next_in_unit(N, ~0u);
+  for (int c = 0; c < C; ++c) {
+    const WalkResult& w = *cones[c];
+    for (uint32_t k = 0; k < w.ops.size(); ++k) {
+      const uint32_t g = base[c] + k;
+      const Op& o = w.ops[k];
+      // the main must be the LAST member: the stage term is then
+      // P_i(s) * X_{i-1}(s) with P_i the left fold of the other members
+      int t_main = -1;
+      if (fuse && o.ns == 1 && o.nin <= kSegMaxNt) {
+        const OpIn& in = w.inputs(o)[o.nin - 1];
+        if (!in.initial && w.ops[in.ref].r == o.width) t_main = o.nin - 1;
+      }
+      if (t_main >= 0) {
+        const uint32_t pg = base[c] + static_cast<uint32_t>(w.inputs(o)[t_main].ref);
+        const Op& p = op_at(pg);
+        const uint32_t u = unit_of[pg];
+        const bool head_ok = unit_len[u] > 1 || (p.ns <= 1 && p.nin <= kSegMaxNt1);
+        const int L = static_cast<int>(unit_len[u]) + 1;
+        if (head_ok && unit_last[u] == pg && L - 1 <= seg_max_j() &&
+            unit_nops[u] + static_cast<uint32_t>(o.nin) <= static_cast<uint32_t>(kSegMaxOps)) {
+          main_pos[g] = static_cast<int8_t>(t_main);
+          unit_of[g] = u;
+          next_in_unit[pg] = g;
+          unit_last[u] = g;
+          ++unit_len[u];
+          unit_nops[u] += static_cast<uint32_t>(o.nin);
+          continue;
+        }
+      }
+      unit_of[g] = static_cast<uint32_t>(unit_first.size());
+      unit_first.push_back(g);
+      unit_last.push_back(g);
+      unit_len.push_back(1);
+      unit_nops.push_back(static_cast<uint32_t>(o.nin));
+    }
+  }
+  const uint32_t U = static_cast<uint32_t>(unit_first.size());
+  // unit levels: 1 + the deepest unit producing a materialised input; units
+  // are visited in the order of their last op (producers come first)
+  std::vector<int32_t> unit_level(U, 0);
+  int max_level = -1;
+  for (int c = 0; c < C; ++c) {
+    const WalkResult& w = *cones[c];
+    for (uint32_t k = 0; k < w.ops.size(); ++k) {
+      const uint32_t g = base[c] + k;
+      const uint32_t u = unit_of[g];
+      if (unit_last[u] != g) continue;
+      int lvl = 0;
+      for (uint32_t s = unit_first[u]; s != ~0u; s = next_in_unit[s]) {
+        const Op& o = op_at(s);
+        const OpIn* ins = w.inputs(o);
+        for (int t = 0; t < o.nin; ++t) {
+          if (ins[t].initial || t == main_pos[s]) continue;
+          lvl = std::max(lvl, unit_level[unit_of[base[c] + static_cast<uint32_t>(ins[t].ref)]] + 1);
+        }
+      }
+      unit_level[u] = lvl;
+      max_level = std::max(max_level, lvl);
+    }
+  }
+  const int n_levels = max_level + 1;
+  auto level_of = [&](uint32_t g) { return unit_level[unit_of[g]]; };
+  auto consumer_unit = [&](uint32_t u) -> int64_t {
+    const Op& o = op_at(unit_last[u]);
+    return o.consumer >= 0 ? static_cast<int64_t>(unit_of[base[lc_of[unit_last[u]]] + o.consumer]) : -1;
+  };
+
+  // stable counting sort of units by level; release lists by consumer level
+  std::vector<uint32_t> lstart(n_levels + 1, 0), order(U);
   std::vector<uint32_t> rstart(n_levels + 1, 0), rel;
   std::vector<uint64_t> level_rows(n_levels, 0);
-  for (uint32_t g = 0; g < N; ++g) {
-    const Op& o = op_at(g);
-    ++lstart[o.level + 1];
-    level_rows[o.level] += o.r > 5 ? uint64_t{1} << (o.r - 5) : 1;
-    if (o.consumer >= 0) ++rstart[cones[lc_of[g]]->ops[o.consumer].level + 1];
+  for (uint32_t u = 0; u < U; ++u) {
+    ++lstart[unit_level[u] + 1];
+    const Op& o = op_at(unit_last[u]);
+    if (unit_len[u] == 1) level_rows[unit_level[u]] += o.r > 5 ? uint64_t{1} << (o.r - 5) : 1;
+    const int64_t cu = consumer_unit(u);
+    if (cu >= 0) ++rstart[unit_level[cu] + 1];
   }
   for (int L = 0; L < n_levels; ++L) {
     lstart[L + 1] += lstart[L];
@@ -113,21 +202,25 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   rel.resize(rstart[n_levels]);
   {
     std::vector<uint32_t> lf(lstart.begin(), lstart.end() - 1), rf(rstart.begin(), rstart.end() - 1);
-    for (uint32_t g = 0; g < N; ++g) {
-      const Op& o = op_at(g);
-      order[lf[o.level]++] = g;
-      if (o.consumer >= 0) rel[rf[cones[lc_of[g]]->ops[o.consumer].level]++] = g;
+    for (uint32_t u = 0; u < U; ++u) {
+      order[lf[unit_level[u]]++] = u;
+      const int64_t cu = consumer_unit(u);
+      if (cu >= 0) rel[rf[unit_level[cu]]++] = u;
     }
   }
 
-  // arena placement over level lifetimes; scalars / kept results live to the end
-  std::vector<uint64_t> out(N);
+  // arena placement of unit outputs over level lifetimes; scalars / kept
+  // results live to the end; fused intermediates get no storage
+  constexpr uint64_t kNoOut = ~uint64_t{0};
+  std::vector<uint64_t> out(N, kNoOut);
   ClassArena arena(round_up(input_elems, kAlign));
-  auto cls_of = [&](uint32_t g) { return std::max<int>(op_at(g).r, kMinClass); };
+  auto cls_of = [&](uint32_t u) { return std::max<int>(op_at(unit_last[u]).r, kMinClass); };
   for (int L = 0; L < n_levels; ++L) {
     if (L > 0)
-      for (uint32_t i = rstart[L - 1]; i < rstart[L]; ++i) arena.release(cls_of(rel[i]), out[rel[i]]);
-    for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) out[order[i]] = arena.alloc(cls_of(order[i]));
+      for (uint32_t i = rstart[L - 1]; i < rstart[L]; ++i)
+        arena.release(cls_of(rel[i]), out[unit_last[rel[i]]]);
+    for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i)
+      out[unit_last[order[i]]] = arena.alloc(cls_of(order[i]));
   }
   hp.arena_elems = arena.peak();
 
@@ -139,7 +232,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     while (row_bits < kItemBits - 5 && (level_rows[L] >> (row_bits + 1)) >= kTargetItems) ++row_bits;
     level_cb[L] = 5 + row_bits;
   }
-  // outer-join classification (DevOp::lead/rb), in parallel
+  // outer-join classification of single-op units (DevOp::lead/rb), in parallel
   std::vector<uint32_t> outer_sig(N, 0);  // 0 = generic; else 1 | lead<<8 | rb0<<16 | rb1<<24
   {
     const int chunks = static_cast<int>(std::min<uint32_t>(N, 256));
@@ -148,8 +241,9 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       std::vector<uint32_t> pm_stamp(max_vars, ~0u);
       for (uint32_t g = static_cast<uint32_t>(uint64_t{N} * ch / chunks);
            g < static_cast<uint32_t>(uint64_t{N} * (ch + 1) / chunks); ++g) {
+        if (unit_len[unit_of[g]] != 1) continue;
         const Op& o = op_at(g);
-        const int cb = std::min<int>(o.r, level_cb[o.level]);
+        const int cb = std::min<int>(o.r, level_cb[level_of(g)]);
         if (!outer_enabled() || o.ns != 1 || o.nin < 2 || o.nin > 4 || cb < 7) continue;
         const WalkResult& w = *cones[lc_of[g]];
         const int32_t* ov = w.out_vars(o);
@@ -174,99 +268,193 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       }
     });
   }
-  // generic ops first, outer-join ops last within each level (stable)
+  // per level: generic single ops, outer-join single ops, segments (stable)
+  auto group_of = [&](uint32_t u) {
+    return unit_len[u] > 1 ? 2 : (outer_sig[unit_last[u]] != 0 ? 1 : 0);
+  };
+  // segments: most expensive tile first (the seg_kernel's dynamic queue then
+  // schedules longest-processing-time first)
+  auto seg_cost = [&](uint32_t u) {
+    return (uint64_t{1} << (unit_len[u] - 1)) * (unit_nops[u] + op_at(unit_first[u]).nin);
+  };
   for (int L = 0; L < n_levels; ++L)
-    std::stable_partition(order.begin() + lstart[L], order.begin() + lstart[L + 1],
-                          [&](uint32_t g) { return outer_sig[g] == 0; });
+    std::stable_sort(order.begin() + lstart[L], order.begin() + lstart[L + 1],
+                     [&](uint32_t a, uint32_t b) {
+                       const int ga = group_of(a), gb = group_of(b);
+                       if (ga != gb) return ga < gb;
+                       return ga == 2 && seg_cost(a) > seg_cost(b);
+                     });
 
-  // descriptors, level by level: the item/tref prefix sums sequentially ...
-  hp.ops.resize(N);
-  hp.ibeg.resize(N);
-  hp.op_width.resize(N);
+  // descriptors, level by level: item/tref prefix sums sequentially ...
+  std::vector<uint32_t> unit_slot(U);   // index into hp.ops or hp.segs
+  std::vector<uint32_t> unit_tref(U);
+  uint32_t n_trefs = 0, n_ops_dev = 0, n_segs = 0, n_stages = 0;
+  for (uint32_t u = 0; u < U; ++u) {
+    if (unit_len[u] == 1) ++n_ops_dev; else { ++n_segs; n_stages += unit_len[u]; }
+  }
+  hp.ops.resize(n_ops_dev);
+  hp.ibeg.resize(n_ops_dev);
+  hp.op_width.resize(n_ops_dev);
+  hp.segs.resize(n_segs);
+  hp.seg_ibeg.resize(n_segs);
+  hp.stages.resize(n_stages);
   hp.level_bytes.assign(n_levels, 0.0);
-  std::vector<double> op_bytes(N);
-  uint32_t n_trefs = 0;
-  for (int L = 0; L < n_levels; ++L) {
-    LevelLaunch ll{lstart[L], 0, 0, 0, 0, 0};
-    for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) {
-      const uint32_t g = order[i];
-      const Op& o = op_at(g);
-      const bool outer = outer_sig[g] != 0;
-      DevOp& d = hp.ops[i];
-      d.out = out[g];
-      d.tref = n_trefs;
-      d.r = static_cast<uint8_t>(o.r);
-      d.ns = static_cast<uint8_t>(o.ns);
-      d.nt = static_cast<uint8_t>(o.nin);
-      d.cb = static_cast<uint8_t>(std::min<int>(o.r, level_cb[L]));
-      d.lead = outer ? static_cast<uint8_t>((outer_sig[g] >> 8) & 0xff) : 0;
-      d.rb[0] = outer ? static_cast<uint8_t>((outer_sig[g] >> 16) & 0xff) : 0;
-      d.rb[1] = outer ? static_cast<uint8_t>(outer_sig[g] >> 24) : 0;
-      uint32_t& items_acc = outer ? ll.outer_items : ll.items;
-      d.item_begin = items_acc;
-      const uint64_t items = uint64_t{1} << (o.r - d.cb);
-      if (items_acc + items > 0xffffffffull) throw Error(kResource, "level has too many work items");
-      items_acc += static_cast<uint32_t>(items);
-      if (outer) {
-        ++ll.outer_count;
-      } else {
-        ++ll.op_count;
-        ll.max_nt = std::max<uint32_t>(ll.max_nt, d.nt);
+  std::vector<uint32_t> unit_stage(U, 0);
+  {
+    uint32_t io = 0, is = 0, ist = 0;
+    for (int L = 0; L < n_levels; ++L) {
+      LevelLaunch ll{io, 0, 0, 0, 0, 0, is, 0, 0};
+      for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) {
+        const uint32_t u = order[i];
+        unit_tref[u] = n_trefs;
+        n_trefs += unit_nops[u];
+        if (unit_len[u] > 1) {
+          const uint32_t g = unit_last[u];
+          const Op& o = op_at(g);
+          DevSeg& sg = hp.segs[is];
+          unit_slot[u] = is++;
+          sg.out = out[g];
+          sg.tref = unit_tref[u];
+          sg.stage = ist;
+          unit_stage[u] = ist;
+          ist += unit_len[u];
+          sg.nst = static_cast<uint8_t>(unit_len[u]);
+          sg.ry = static_cast<uint8_t>(o.r);
+          sg.cy = static_cast<uint8_t>(std::min<int>(o.r, kSegYBits));
+          sg.nops = static_cast<uint8_t>(unit_nops[u]);
+          sg.item_begin = ll.seg_items;
+          hp.seg_ibeg[is - 1] = ll.seg_items;
+          const uint64_t tiles = uint64_t{1} << (o.r - sg.cy);
+          if (ll.seg_items + tiles > 0xffffffffull) throw Error(kResource, "level has too many tiles");
+          ll.seg_items += static_cast<uint32_t>(tiles);
+          ++ll.seg_count;
+          continue;
+        }
+        const uint32_t g = unit_last[u];
+        const Op& o = op_at(g);
+        const bool outer = outer_sig[g] != 0;
+        DevOp& d = hp.ops[io];
+        unit_slot[u] = io;
+        d.out = out[g];
+        d.tref = unit_tref[u];
+        d.r = static_cast<uint8_t>(o.r);
+        d.ns = static_cast<uint8_t>(o.ns);
+        d.nt = static_cast<uint8_t>(o.nin);
+        d.cb = static_cast<uint8_t>(std::min<int>(o.r, level_cb[L]));
+        d.lead = outer ? static_cast<uint8_t>((outer_sig[g] >> 8) & 0xff) : 0;
+        d.rb[0] = outer ? static_cast<uint8_t>((outer_sig[g] >> 16) & 0xff) : 0;
+        d.rb[1] = outer ? static_cast<uint8_t>(outer_sig[g] >> 24) : 0;
+        uint32_t& items_acc = outer ? ll.outer_items : ll.items;
+        d.item_begin = items_acc;
+        const uint64_t items = uint64_t{1} << (o.r - d.cb);
+        if (items_acc + items > 0xffffffffull) throw Error(kResource, "level has too many work items");
+        items_acc += static_cast<uint32_t>(items);
+        if (outer) {
+          ++ll.outer_count;
+        } else {
+          ++ll.op_count;
+          ll.max_nt = std::max<uint32_t>(ll.max_nt, d.nt);
+        }
+        hp.ibeg[io] = d.item_begin;
+        hp.op_width[io] = o.bucket_seq >= 0 ? o.width : 0;
+        ++io;
       }
-      hp.ibeg[i] = d.item_begin;
-      hp.op_width[i] = o.bucket_seq >= 0 ? o.width : 0;
-      n_trefs += static_cast<uint32_t>(o.nin);
+      hp.levels.push_back(ll);
     }
-    hp.levels.push_back(ll);
   }
   // ... then every operand's bit map in parallel chunks
   hp.trefs.resize(n_trefs);
-  const int chunks = static_cast<int>(std::min<uint32_t>(N, 256));
+  std::vector<double> op_bytes(N, 0.0), unit_dev_bytes(U, 0.0);
+  const int chunks = static_cast<int>(std::min<uint32_t>(U, 256));
   std::vector<int> chunk_err(chunks, 0);
   Pool::get().parallel_for(chunks, [&](int ch) {
-    const uint32_t i0 = static_cast<uint32_t>(uint64_t{N} * ch / chunks);
-    const uint32_t i1 = static_cast<uint32_t>(uint64_t{N} * (ch + 1) / chunks);
+    const uint32_t u0 = static_cast<uint32_t>(uint64_t{U} * ch / chunks);
+    const uint32_t u1 = static_cast<uint32_t>(uint64_t{U} * (ch + 1) / chunks);
     std::vector<uint8_t> pm(max_vars);
     std::vector<uint32_t> pm_stamp(max_vars, ~0u);
-    for (uint32_t i = i0; i < i1; ++i) {
-      const uint32_t g = order[i];
-      const WalkResult& w = *cones[lc_of[g]];
-      const Op& o = op_at(g);
-      const uint32_t cb0 = base[lc_of[g]];
-      DevOp& d = hp.ops[i];
-      const int r = o.r, ns = o.ns;
-      // output var -> bit (LSB-indexed), summed var -> kSumSrc + j
-      const int32_t* ov = w.out_vars(o);
-      const int32_t* sv = w.sum_vars(o);
-      for (int k = 0; k < r; ++k) { pm[ov[k]] = static_cast<uint8_t>(r - 1 - k); pm_stamp[ov[k]] = g; }
-      for (int k = 0; k < ns; ++k) { pm[sv[k]] = static_cast<uint8_t>(kSumSrc + ns - 1 - k); pm_stamp[sv[k]] = g; }
-      double bytes = 16.0 * static_cast<double>(uint64_t{1} << r);
-      const OpIn* ins = w.inputs(o);
-      for (int t = 0; t < o.nin; ++t) {
-        const OpIn& in = ins[t];
-        if (in.rank > kMaxRank) { chunk_err[ch] = 1; return; }
-        DevTensor& x = hp.trefs[d.tref + t];
-        x = DevTensor{};
-        x.off = in.initial ? static_cast<uint64_t>(in.ref) : out[cb0 + in.ref];
-        x.rank = static_cast<uint8_t>(in.rank);
-        const int32_t* iv = w.in_vars(in);
-        for (int ax = 0; ax < in.rank; ++ax) {
-          if (pm_stamp[iv[ax]] != g) { chunk_err[ch] = 2; return; }
-          x.src[ax] = pm[iv[ax]];
-        }
-        bytes += 16.0 * static_cast<double>(uint64_t{1} << in.rank);
+    uint32_t stamp = 0;
+    for (uint32_t u = u0; u < u1; ++u) {
+      const uint32_t c = lc_of[unit_first[u]];
+      const WalkResult& w = *cones[c];
+      const uint32_t cb0 = base[c];
+      const Op& last = op_at(unit_last[u]);
+      const bool seg = unit_len[u] > 1;
+      ++stamp;
+      // var -> code.  Single op: output bit (LSB-indexed) / kSumSrc + j.
+      // Segment: Y bit -> in-tile or tile-number bit; digit s_k -> in-tile bit
+      const int ry = last.r, cy = std::min<int>(ry, kSegYBits);
+      const int32_t* ov = w.out_vars(last);
+      for (int k = 0; k < ry; ++k) {
+        const int b = ry - 1 - k;
+        pm[ov[k]] = static_cast<uint8_t>(!seg ? b : (b < cy ? b : kTileSrc + (b - cy)));
+        pm_stamp[ov[k]] = stamp;
       }
-      mark_invariant_lead(d, hp.trefs.data() + d.tref);
-      op_bytes[g] = bytes;
+      double dev_bytes = 16.0 * static_cast<double>(uint64_t{1} << ry);
+      uint32_t tix = unit_tref[u];
+      int stage = 0;
+      for (uint32_t g = unit_first[u]; g != ~0u; g = next_in_unit[g], ++stage) {
+        const Op& o = op_at(g);
+        const int32_t* sv = w.sum_vars(o);
+        // own summed vars; in a segment, stage i >= 2 sums digit s_i = j bit i-2
+        for (int k = 0; k < o.ns; ++k) {
+          pm[sv[k]] = static_cast<uint8_t>(seg && stage > 0 ? kJSrc + (stage - 1) : kSumSrc + o.ns - 1 - k);
+          pm_stamp[sv[k]] = stamp;
+        }
+        if (seg) {
+          // digits of the later stages: s_k (1-based k = stage + 2 .. L) = j bit k-2
+          uint32_t h = next_in_unit[g];
+          for (int k = stage + 2; h != ~0u; h = next_in_unit[h], ++k) {
+            const Op& oh = op_at(h);
+            const int32_t v = w.sum_vars(oh)[0];
+            pm[v] = static_cast<uint8_t>(kJSrc + (k - 2));
+            pm_stamp[v] = stamp;
+          }
+          DevStage& st = hp.stages[unit_stage[u] + stage];
+          st.nt = static_cast<uint8_t>(o.nin);
+          st.main = stage == 0 ? kSegMain : static_cast<uint8_t>(main_pos[g]);
+          st.ns = static_cast<uint8_t>(o.ns);
+          st.op0 = static_cast<uint8_t>(tix - unit_tref[u]);
+        }
+        double bytes = 16.0 * static_cast<double>(uint64_t{1} << o.r);
+        const OpIn* ins = w.inputs(o);
+        for (int t = 0; t < o.nin; ++t, ++tix) {
+          const OpIn& in = ins[t];
+          bytes += 16.0 * static_cast<double>(uint64_t{1} << in.rank);
+          DevTensor& x = hp.trefs[tix];
+          x = DevTensor{};
+          if (seg && t == main_pos[g]) continue;  // placeholder: read from shared memory
+          dev_bytes += 16.0 * static_cast<double>(uint64_t{1} << in.rank);
+          if (in.rank > kMaxRank) { chunk_err[ch] = 1; return; }
+          x.off = in.initial ? static_cast<uint64_t>(in.ref) : out[cb0 + in.ref];
+          if (x.off == kNoOut) { chunk_err[ch] = 3; return; }
+          x.rank = static_cast<uint8_t>(in.rank);
+          const int32_t* iv = w.in_vars(in);
+          for (int ax = 0; ax < in.rank; ++ax) {
+            if (pm_stamp[iv[ax]] != stamp) { chunk_err[ch] = 2; return; }
+            x.src[ax] = pm[iv[ax]];
+          }
+        }
+        op_bytes[g] = bytes;
+        // the summed vars of this stage never reappear
+        if (seg) for (int k = 0; k < o.ns; ++k) pm_stamp[sv[k]] = 0;
+      }
+      if (!seg) {
+        DevOp& d = hp.ops[unit_slot[u]];
+        mark_invariant_lead(d, hp.trefs.data() + d.tref);
+      }
+      unit_dev_bytes[u] = dev_bytes;
     }
   });
   for (int e : chunk_err) {
     if (e == 1) throw Error(kResource, "tensor rank exceeds the device limit " + std::to_string(kMaxRank));
     if (e == 2) throw Error(kSchedule, "internal: operand var outside its bucket");
+    if (e == 3) throw Error(kSchedule, "internal: operand reads a fused intermediate");
   }
-  for (int L = 0; L < n_levels; ++L)
-    for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) {
-      const uint32_t g = order[i];
+  for (uint32_t u = 0; u < U; ++u) {
+    const int L = unit_level[u];
+    hp.dev_bytes += unit_dev_bytes[u];
+    if (unit_len[u] > 1) hp.n_fused_ops += unit_len[u];
+    for (uint32_t g = unit_first[u]; g != ~0u; g = next_in_unit[g]) {
       const Op& o = op_at(g);
       hp.level_bytes[L] += op_bytes[g];
       hp.alg_bytes += op_bytes[g];
@@ -276,6 +464,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
         hp.max_width = std::max(hp.max_width, static_cast<int>(o.width));
       }
     }
+  }
 
   // records (one per non-empty bucket, walk order) and per-lightcone scalars
   hp.rec_begin.reserve(C + 1);
@@ -289,7 +478,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       if (o.bucket_seq < 0) continue;
       hp.rec_seq.push_back(o.bucket_seq);
       hp.rec_width.push_back(o.width);
-      hp.rec_level.push_back(o.level);
+      hp.rec_level.push_back(level_of(base[c] + k));
       hp.rec_bytes.push_back(op_bytes[base[c] + k]);
       hp.rec_out.push_back(out[base[c] + k]);
     }

@@ -17,7 +17,14 @@ struct HostPlan {
   std::vector<uint32_t> ibeg;          // ops[i].item_begin, contiguous (kernel lookup table)
   std::vector<int32_t> op_width;       // bucket width per device op, 0 for pre-fold helpers
   std::vector<DevTensor> trefs;
+  std::vector<DevSeg> segs;            // fused-chain segments, level-sorted
+  std::vector<uint32_t> seg_ibeg;      // segs[i].item_begin, contiguous
+  std::vector<DevStage> stages;
   std::vector<LevelLaunch> levels;
+  // HBM bytes the device program must move (fused intermediates excluded):
+  // per unit sum of its materialised inputs + its output
+  double dev_bytes = 0;
+  uint64_t n_fused_ops = 0;            // ops evaluated inside segments
   std::vector<uint64_t> scalar_off;    // per lightcone: its scalar results, production order
   std::vector<uint32_t> lc_begin;      // n_lightcones + 1 prefix into scalar_off
   uint64_t input_elems = 0;
@@ -36,8 +43,14 @@ struct HostPlan {
   std::vector<uint64_t> rec_out;       // arena offset of each recorded op's result
 };
 
+// Default for build_plan's `fuse`: on unless QTNG_FUSE=0.
+bool fuse_default();
+
 // Plans `cones` (each the walk of one lightcone's schedule) onto one arena
-// whose first `input_elems` elements hold the inputs.
-HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems);
+// whose first `input_elems` elements hold the inputs.  Chains of buckets whose
+// intermediate spans the consumer's whole width become fused segments;
+// fuse=false keeps every op a separate level-kernel op (no chain fusion).
+HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems,
+                    bool fuse = fuse_default());
 
 }  // namespace qtng
