@@ -152,7 +152,7 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
 // Descriptor image of a HostPlan: one contiguous blob, 256-byte aligned sections.
 struct DescLayout {
   size_t ops = 0, ibeg = 0, trefs = 0, segs = 0, seg_ibeg = 0, stages = 0, ctr = 0, scal = 0,
-         lcb = 0, terms = 0, total = 0;
+         lcb = 0, terms = 0, upload = 0, segtab = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t{255}; }
@@ -170,6 +170,8 @@ DescLayout layout_of(const HostPlan& hp) {
   L.scal = o; o = align256(o + hp.scalar_off.size() * sizeof(uint64_t));
   L.lcb = o; o = align256(o + hp.lc_begin.size() * sizeof(uint32_t));
   L.terms = o; o = align256(o + (hp.lc_begin.size()) * sizeof(double2));
+  L.upload = o;  // device-only sections follow
+  L.segtab = o; o = align256(o + (hp.segs.empty() ? 0 : hp.trefs.size() * sizeof(SegOpTab)));
   L.total = o;
   return L;
 }
@@ -229,6 +231,7 @@ struct DevProgram {
   const DevSeg* segs() const { return reinterpret_cast<const DevSeg*>(base + L.segs); }
   const uint32_t* seg_ibeg() const { return reinterpret_cast<const uint32_t*>(base + L.seg_ibeg); }
   const DevStage* stages() const { return reinterpret_cast<const DevStage*>(base + L.stages); }
+  SegOpTab* segtab() const { return reinterpret_cast<SegOpTab*>(base + L.segtab); }
   uint32_t* ctr(size_t level) const { return reinterpret_cast<uint32_t*>(base + L.ctr) + 2 * level; }
   const uint64_t* scal() const { return reinterpret_cast<const uint64_t*>(base + L.scal); }
   const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
@@ -249,16 +252,27 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
   }
   if (fork3) {
     QTNG_CUDA(cudaStreamWaitEvent(ctx->stream3, ctx->fork_ev, 0));
-    QTNG_CUDA(launch_segs(ctx->stream3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(), arena,
+    QTNG_CUDA(launch_segs(ctx->stream3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.segtab(), arena,
                           pr.ctr(level), lv));
     QTNG_CUDA(cudaEventRecord(ctx->join3_ev, ctx->stream3));
   } else {
-    QTNG_CUDA(launch_segs(ctx->stream, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(), arena,
+    QTNG_CUDA(launch_segs(ctx->stream, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.segtab(), arena,
                           pr.ctr(level), lv));
   }
   QTNG_CUDA(launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
   if (fork2) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join3_ev, 0));
+}
+
+// Upload a HostPlan's descriptor image to `dev` (layout L) on the context
+// stream and build its device-only segment tables.
+void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* dev) {
+  ctx->pin_desc.ensure(L.upload);
+  pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
+  QTNG_CUDA(cudaMemcpyAsync(dev, ctx->pin_desc.p, L.upload, cudaMemcpyHostToDevice, ctx->stream));
+  const DevProgram pr{dev, L};
+  QTNG_CUDA(launch_seg_prep(ctx->stream, pr.segs(), static_cast<uint32_t>(hp.segs.size()), pr.trefs(),
+                            pr.segtab()));
 }
 
 // Enqueue the whole program on the context's stream: every level, then the
@@ -486,14 +500,11 @@ void run_program_once(qtng_ctx* ctx, const HostPlan& hp, const double* input,
   const DescLayout L = layout_of(hp);
   ctx->ensure_arena(std::max(hp.arena_elems, input_elems));
   ctx->desc.ensure(L.total);
-  ctx->pin_desc.ensure(L.total);
-  pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
   ctx->pin_in.ensure(std::max<uint64_t>(input_elems, 1) * sizeof(double2));
   std::memcpy(ctx->pin_in.p, input, input_elems * sizeof(double2));
   QTNG_CUDA(cudaMemcpyAsync(ctx->A(), ctx->pin_in.p, input_elems * sizeof(double2),
                             cudaMemcpyHostToDevice, ctx->stream));
-  QTNG_CUDA(cudaMemcpyAsync(ctx->desc.p, ctx->pin_desc.p, L.total, cudaMemcpyHostToDevice,
-                            ctx->stream));
+  upload_desc(ctx, hp, L, static_cast<char*>(ctx->desc.p));
   DevProgram pr{static_cast<char*>(ctx->desc.p), L};
   enqueue_program(ctx, hp, pr, ctx->A(), nullptr);
   if (terms_host) {
@@ -623,10 +634,7 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
     QTNG_CUDA(cudaSetDevice(ctx->device));
     plan->desc.ensure(L.total);
     plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L};
-    ctx->pin_desc.ensure(L.total);
-    pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
-    QTNG_CUDA(cudaMemcpyAsync(plan->desc.p, ctx->pin_desc.p, L.total, cudaMemcpyHostToDevice,
-                              ctx->stream));
+    upload_desc(ctx, hp, L, static_cast<char*>(plan->desc.p));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     plan->pin_gate.ensure(hp.input_elems * sizeof(double2));
     plan->pin_terms.ensure(std::max<size_t>(1, cs.walks.size()) * sizeof(double2));
@@ -661,10 +669,7 @@ qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* i
     QTNG_CUDA(cudaSetDevice(ctx->device));
     plan->desc.ensure(L.total);
     plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L};
-    ctx->pin_desc.ensure(L.total);
-    pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
-    QTNG_CUDA(cudaMemcpyAsync(plan->desc.p, ctx->pin_desc.p, L.total, cudaMemcpyHostToDevice,
-                              ctx->stream));
+    upload_desc(ctx, hp, L, static_cast<char*>(plan->desc.p));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     plan->pin_gate.ensure(std::max<uint64_t>(input_elems, 1) * sizeof(double2));
     std::memcpy(plan->pin_gate.p, data, input_elems * sizeof(double2));
@@ -748,7 +753,7 @@ void fill_info(const HostPlan& hp, int n_lightcones, qtng_plan_info* info) {
     info->alg_bytes = hp.alg_bytes;
     info->sum_ops = hp.sum_ops;
     info->arena_bytes = hp.arena_elems * sizeof(double2);
-    info->desc_bytes = layout_of(hp).total;
+    info->desc_bytes = layout_of(hp).upload;
     info->kernels_per_run = launches_per_run(hp);
     info->n_segments = hp.segs.size();
     info->n_fused_ops = hp.n_fused_ops;

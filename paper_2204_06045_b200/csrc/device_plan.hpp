@@ -94,6 +94,22 @@ struct alignas(16) DevSeg {
 };
 static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
 
+// Per-operand tables of a segment, built on the device once per plan upload
+// (seg_prep_kernel) from the DevTensor bit maps and read by seg_kernel through
+// the read-only path.  Indexed like the DevTensor array.
+struct alignas(16) SegOpTab {
+  uint64_t off;                // arena element offset
+  uint32_t sd;                 // stage 1: offset of its own summed bit
+  uint32_t pad;
+  uint32_t dj[kSegMaxJ];       // offset per digit bit
+  uint32_t inc[kSegMaxJ];      // offset step from j-1 to j when bit b is the lowest set bit of j
+  uint32_t dlo[16];            // subset sums of digit bits 0..3
+  uint32_t dhi[16];            // subset sums of digit bits 4..7
+  uint32_t dtile[32];          // offset per tile-number bit
+  uint32_t llane[32];          // lane part of the offset, per lane
+};
+static_assert(sizeof(SegOpTab) == 464, "SegOpTab layout");
+
 struct DevStage {
   uint8_t nt;    // members (bucket member order)
   uint8_t main;  // position of the main member (kSegMain for stage 1)

@@ -391,92 +391,91 @@ outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
 // register file, no barrier is needed, and every X_i element is produced by
 // the unfused bucket's exact operation sequence (left-fold product in member
 // order, ascending summed values), so results are bit-identical.
-struct ChainWarp {
-  uint64_t off[kSegMaxOps];              // arena offset of each operand
-  uint32_t llane[kSegMaxOps][32];        // lane part of the operand offset
-  uint32_t base[kSegMaxOps][32];         // lane + current tile part
-  uint32_t dtile[kSegMaxOps][32];        // delta per tile-number bit
-  uint32_t dj[kSegMaxOps][kSegMaxJ];     // delta per j bit
-  uint32_t inc[kSegMaxOps][kSegMaxJ];    // stage 1: offset step when j increments past bit b
-  uint32_t dlo[kSegMaxOps][16];          // offset of j bits 0..3
-  uint32_t dhi[kSegMaxOps][16];          // offset of j bits 4..7
-  uint32_t sd[kSegMaxOps];               // stage 1: offset of its summed bit
-  DevStage st[kSegMaxStages];
-  double2 acc[kSegMaxStages - 3][32];    // per lane: parked s_i = 0 terms of stages >= 4
-};
-
-// Per-segment operand tables (one warp).
-__device__ void chain_decode(ChainWarp& cw, const DevSeg& sg, const DevStage* __restrict__ stages,
-                             const DevTensor* __restrict__ trefs, int lane) {
-  __syncwarp();
-  if (lane < sg.nst) cw.st[lane] = stages[sg.stage + lane];
+// seg_prep_kernel: one warp per segment fills the SegOpTab of each operand.
+__global__ void seg_prep_kernel(const DevSeg* __restrict__ segs, uint32_t n_segs,
+                                const DevTensor* __restrict__ trefs, SegOpTab* __restrict__ tab) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_segs) return;
+  const DevSeg sg = segs[w];
   for (int op = 0; op < sg.nops; ++op) {
     const DevTensor* d = trefs + sg.tref + op;
+    SegOpTab& t = tab[sg.tref + op];
     const int rank = d->rank;
-    uint32_t lv = 0, dt = 0, s = 0, dj = 0;  // lane: own part; lane b: tile bit b / j bit b delta
+    uint32_t lv = 0, dt = 0, s = 0, dj = 0;  // lane: own part; lane b: tile bit b / digit bit b
     for (int ax = 0; ax < rank; ++ax) {
-      const uint32_t code = __ldg(&d->src[ax]);
+      const uint32_t code = d->src[ax];
       const uint32_t bit = 1u << (rank - 1 - ax);
       if (code < kLaneSrcEnd) lv |= ((lane >> code) & 1u) ? bit : 0u;
       else if (code < kTileSrc) dj |= (code - kJSrc == static_cast<uint32_t>(lane)) ? bit : 0u;
       else if (code < kSumSrc) dt |= (code - kTileSrc == static_cast<uint32_t>(lane)) ? bit : 0u;
       else s = bit;
     }
-    cw.llane[op][lane] = lv;
-    cw.dtile[op][lane] = dt;
-    if (lane < kSegMaxJ) cw.dj[op][lane] = dj;
-    // inc[b] = dj[b] - sum_{b' < b} dj[b'];  dlo/dhi: subset sums of j bits 0..3 / 4..7
+    t.llane[lane] = lv;
+    t.dtile[lane] = dt;
+    if (lane < kSegMaxJ) t.dj[lane] = dj;
     uint32_t below = 0;
     for (int b = 0; b < kSegMaxJ; ++b) {
       const uint32_t djb = __shfl_sync(kFull, dj, b);
-      if (lane == b) cw.inc[op][b] = djb - below;
+      if (lane == b) t.inc[b] = djb - below;
       below += djb;
     }
     uint32_t lo = 0, hi = 0;
-    for (int b = 0; b < 4; ++b) {  // every lane takes part in the shuffles
+    for (int b = 0; b < 4; ++b) {
       const uint32_t xl = __shfl_sync(kFull, dj, b), xh = __shfl_sync(kFull, dj, b + 4);
       lo += ((lane >> b) & 1) ? xl : 0u;
       hi += ((lane >> b) & 1) ? xh : 0u;
     }
     if (lane < 16) {
-      cw.dlo[op][lane] = lo;
-      cw.dhi[op][lane] = hi;
+      t.dlo[lane] = lo;
+      t.dhi[lane] = hi;
     }
     if (lane == 0) {
-      cw.sd[op] = s;
-      cw.off[op] = d->off;
+      t.sd = s;
+      t.off = d->off;
     }
   }
-  __syncwarp();
 }
+
+// Per-warp state of seg_kernel: the current tile's offsets and the parked terms.
+struct ChainWarp {
+  uint32_t toff[kSegMaxOps];             // tile part of each operand's offset
+  DevStage st[kSegMaxStages];
+  double2 acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
+};
 
 // Side-member product P_i (left fold of members [op0, op0+m)) at digit
 // assignment j; m >= 1.
-__device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const double2* __restrict__ arena,
-                                              int op0, int m, uint32_t j, int lane) {
+__device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                              const double2* __restrict__ arena, int op0, int m,
+                                              uint32_t j, int lane) {
   const uint32_t jl = j & 15u, jh = j >> 4;
   double2 p = make_double2(0.0, 0.0);
   for (int t = 0; t < m; ++t) {
     const int op = op0 + t;
-    const double2 x = ld(arena + cw.off[op] + (cw.base[op][lane] + cw.dlo[op][jl] + cw.dhi[op][jh]));
+    const SegOpTab* tb = tab + op;
+    const double2 x = ld(arena + __ldg(&tb->off) +
+                         (cw.toff[op] + __ldg(&tb->llane[lane]) + __ldg(&tb->dlo[jl]) + __ldg(&tb->dhi[jh])));
     p = t == 0 ? x : cmul(p, x);
   }
   return p;
 }
 
 // term of stage i (DevStage st) at digit assignment j: P_i(j) * v, or v.
-__device__ __forceinline__ double2 chain_term(const ChainWarp& cw, const double2* __restrict__ arena,
-                                              const DevStage st, uint32_t j, double2 v, int lane) {
+__device__ __forceinline__ double2 chain_term(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                              const double2* __restrict__ arena, const DevStage st,
+                                              uint32_t j, double2 v, int lane) {
   const int m = st.nt - 1;
-  return m ? cmul(chain_side(cw, arena, st.op0, m, j, lane), v) : v;
+  return m ? cmul(chain_side(cw, tab, arena, st.op0, m, j, lane), v) : v;
 }
 
 // One tile: 2^J stage-1 evaluations (NT members, NS summed bits), in groups
 // of 2^U consecutive j (stages 2..U+1 resolved in registers, four independent
 // stage-1 products in flight), then the climb above each group.
 template <int NT, int NS, int U>
-__device__ __forceinline__ void chain_tile(ChainWarp& cw, const DevSeg& sg,
-                                           double2* __restrict__ arena, uint32_t tile, int lane) {
+__device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                           const DevSeg& sg, double2* __restrict__ arena,
+                                           uint32_t tile, int lane) {
   constexpr int G = 1 << U;
   const int L = sg.nst;
   const uint32_t nj = 1u << (L - 1);
@@ -484,11 +483,11 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const DevSeg& sg,
   uint32_t o[NT], sdl[NT], d0[NT], d1[NT];
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
-    B[t] = arena + cw.off[t];
-    o[t] = cw.base[t][lane];
-    sdl[t] = cw.sd[t];
-    d0[t] = cw.dj[t][0];
-    d1[t] = U > 1 ? cw.dj[t][1] : 0u;
+    B[t] = arena + __ldg(&tab[t].off);
+    o[t] = cw.toff[t] + __ldg(&tab[t].llane[lane]);
+    sdl[t] = __ldg(&tab[t].sd);
+    d0[t] = __ldg(&tab[t].dj[0]);
+    d1[t] = U > 1 ? __ldg(&tab[t].dj[1]) : 0u;
   }
   const DevStage st2 = cw.st[1];
   const DevStage st3 = U > 1 ? cw.st[2] : st2;
@@ -496,7 +495,7 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const DevSeg& sg,
     if (j) {  // from j - G (low U bits clear) to j: inc[b] assumes bits < b were set
       const int b = __ffs(j) - 1;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) o[t] += cw.inc[t][b] + d0[t] + d1[t];
+      for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t] + d1[t];
     }
     double2 v[G];
 #pragma unroll
@@ -516,33 +515,35 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const DevSeg& sg,
       v[q] = x;
     }
     // stage 2 over bit 0, stage 3 over bit 1 (U == 2)
-    double2 x = cadd(chain_term(cw, arena, st2, j, v[0], lane), chain_term(cw, arena, st2, j | 1u, v[1], lane));
+    double2 x = cadd(chain_term(cw, tab, arena, st2, j, v[0], lane), chain_term(cw, tab, arena, st2, j | 1u, v[1], lane));
     if (U > 1) {
-      const double2 y = cadd(chain_term(cw, arena, st2, j | 2u, v[2], lane),
-                             chain_term(cw, arena, st2, j | 3u, v[3], lane));
-      x = cadd(chain_term(cw, arena, st3, j, x, lane), chain_term(cw, arena, st3, j | 2u, y, lane));
+      const double2 y = cadd(chain_term(cw, tab, arena, st2, j | 2u, v[2], lane),
+                             chain_term(cw, tab, arena, st2, j | 3u, v[3], lane));
+      x = cadd(chain_term(cw, tab, arena, st3, j, x, lane), chain_term(cw, tab, arena, st3, j | 2u, y, lane));
     }
     // climb: stage i = k + 2 >= U + 2 while the carry propagates
     const uint32_t jj = j | (G - 1);
     bool carry = true;
     for (int k = U; k + 2 <= L; ++k) {
-      const double2 term = chain_term(cw, arena, cw.st[k + 1], jj, x, lane);
+      const double2 term = chain_term(cw, tab, arena, cw.st[k + 1], jj, x, lane);
       if (!((jj >> k) & 1u)) {
-        cw.acc[k - 2][lane] = term;
+        cw.acc[k - 1][lane] = term;
         carry = false;
         break;
       }
-      x = cadd(cw.acc[k - 2][lane], term);
+      x = cadd(cw.acc[k - 1][lane], term);
     }
     if (carry && lane < (1 << sg.cy)) arena[sg.out + (static_cast<uint64_t>(tile) << sg.cy) + lane] = x;
   }
 }
 
 template <int NT, int NS>
-__device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const DevSeg& sg, double2* __restrict__ arena,
+__device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                             const DevSeg& sg, double2* __restrict__ arena,
                                              uint32_t tile, int lane) {
-  if (sg.nst >= 3) chain_tile<NT, NS, 2>(cw, sg, arena, tile, lane);
-  else chain_tile<NT, NS, 1>(cw, sg, arena, tile, lane);
+  // wide heads use pairs of j (register pressure), the rest groups of four
+  if (NT <= 4 && sg.nst >= 3) chain_tile<NT, NS, (NT <= 4 ? 2 : 1)>(cw, tab, sg, arena, tile, lane);
+  else chain_tile<NT, NS, 1>(cw, tab, sg, arena, tile, lane);
 }
 
 #ifndef QTNG_SEG_MINB
@@ -550,7 +551,7 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const DevSeg& sg, do
 #endif
 __global__ void __launch_bounds__(32, QTNG_SEG_MINB)
 seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
-           const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
+           const DevStage* __restrict__ stages, const SegOpTab* __restrict__ segtab,
            double2* __restrict__ arena, uint32_t seg_count, uint32_t items, uint32_t* ctr) {
   __shared__ ChainWarp cw;
   const int lane = threadIdx.x;
@@ -573,31 +574,34 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
       if (static_cast<int>(lo) != cur) {
         cur = static_cast<int>(lo);
         sg = segs[lo];
-        chain_decode(cw, sg, stages, trefs, lane);
+        __syncwarp();
+        if (lane < sg.nst) cw.st[lane] = stages[sg.stage + lane];
       }
       cur_begin = __ldg(ibeg + lo);
       cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
     }
     const uint32_t tile = item - cur_begin;
+    const SegOpTab* tab = segtab + sg.tref;
     for (int op = 0; op < sg.nops; ++op) {
-      const uint32_t v = ((tile >> lane) & 1u) ? cw.dtile[op][lane] : 0u;
-      cw.base[op][lane] = cw.llane[op][lane] + __reduce_add_sync(kFull, v);
+      const uint32_t v = ((tile >> lane) & 1u) ? __ldg(&tab[op].dtile[lane]) : 0u;
+      const uint32_t sum = __reduce_add_sync(kFull, v);
+      if (lane == 0) cw.toff[op] = sum;
     }
     __syncwarp();
     const DevStage s1 = cw.st[0];
     switch (s1.nt * 2 + s1.ns) {
-      case 2: chain_tile_u<1, 0>(cw, sg, arena, tile, lane); break;
-      case 3: chain_tile_u<1, 1>(cw, sg, arena, tile, lane); break;
-      case 4: chain_tile_u<2, 0>(cw, sg, arena, tile, lane); break;
-      case 5: chain_tile_u<2, 1>(cw, sg, arena, tile, lane); break;
-      case 6: chain_tile_u<3, 0>(cw, sg, arena, tile, lane); break;
-      case 7: chain_tile_u<3, 1>(cw, sg, arena, tile, lane); break;
-      case 8: chain_tile_u<4, 0>(cw, sg, arena, tile, lane); break;
-      case 9: chain_tile_u<4, 1>(cw, sg, arena, tile, lane); break;
-      case 10: chain_tile_u<5, 0>(cw, sg, arena, tile, lane); break;
-      case 11: chain_tile_u<5, 1>(cw, sg, arena, tile, lane); break;
-      case 12: chain_tile_u<6, 0>(cw, sg, arena, tile, lane); break;
-      default: chain_tile_u<6, 1>(cw, sg, arena, tile, lane); break;
+      case 2: chain_tile_u<1, 0>(cw, tab, sg, arena, tile, lane); break;
+      case 3: chain_tile_u<1, 1>(cw, tab, sg, arena, tile, lane); break;
+      case 4: chain_tile_u<2, 0>(cw, tab, sg, arena, tile, lane); break;
+      case 5: chain_tile_u<2, 1>(cw, tab, sg, arena, tile, lane); break;
+      case 6: chain_tile_u<3, 0>(cw, tab, sg, arena, tile, lane); break;
+      case 7: chain_tile_u<3, 1>(cw, tab, sg, arena, tile, lane); break;
+      case 8: chain_tile_u<4, 0>(cw, tab, sg, arena, tile, lane); break;
+      case 9: chain_tile_u<4, 1>(cw, tab, sg, arena, tile, lane); break;
+      case 10: chain_tile_u<5, 0>(cw, tab, sg, arena, tile, lane); break;
+      case 11: chain_tile_u<5, 1>(cw, tab, sg, arena, tile, lane); break;
+      case 12: chain_tile_u<6, 0>(cw, tab, sg, arena, tile, lane); break;
+      default: chain_tile_u<6, 1>(cw, tab, sg, arena, tile, lane); break;
     }
     __syncwarp();
   }
@@ -677,12 +681,19 @@ cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
   return cudaGetLastError();
 }
 
+cudaError_t launch_seg_prep(cudaStream_t s, const DevSeg* segs, uint32_t n_segs,
+                            const DevTensor* trefs, SegOpTab* segtab) {
+  if (n_segs == 0) return cudaSuccess;
+  seg_prep_kernel<<<(n_segs + 3) / 4, 128, 0, s>>>(segs, n_segs, trefs, segtab);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
-                        const DevStage* stages, const DevTensor* trefs, double2* arena,
+                        const DevStage* stages, const SegOpTab* segtab, double2* arena,
                         uint32_t* ctr, const LevelLaunch& lv) {
   if (lv.seg_items == 0) return cudaSuccess;
   seg_kernel<<<seg_grid(lv.seg_items), 32, 0, s>>>(
-      segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, trefs, arena, lv.seg_count,
+      segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, segtab, arena, lv.seg_count,
       lv.seg_items, ctr);
   return cudaGetLastError();
 }
