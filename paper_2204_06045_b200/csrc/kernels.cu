@@ -547,7 +547,7 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
 }
 
 #ifndef QTNG_SEG_MINB
-#define QTNG_SEG_MINB 20  // resident one-warp CTAs per SM the register budget must allow
+#define QTNG_SEG_MINB 32  // resident one-warp CTAs per SM (tuned: 32 = the per-SM block limit)
 #endif
 __global__ void __launch_bounds__(32, QTNG_SEG_MINB)
 seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,

@@ -17,9 +17,15 @@ L, by, lms = plan.time_level(-1, 20)
 print(json.dumps(dict(ms_step=ms, level_sum=float(lv.sum()), big_level=L, big_gbs=by/lms/1e6, energy=e,
                       top=[round(float(x),1) for x in sorted(lv*1e3)[-6:]])))
 ''' % ROOT
+# env sweeps: "NAME=v1,v2;NAME2=..." (default: one run per variant)
+sweep = [[]]
+for part in (sys.argv[1] if len(sys.argv) > 1 else "").split(";"):
+    if "=" in part:
+        k, vs = part.split("=", 1)
+        sweep = [s + [(k, v)] for s in sweep for v in vs.split(",")]
 for so in sorted(glob.glob(os.path.join(ROOT, "build/variants/*.so"))):
-    for rt in ("0", "1"):
-        env = dict(os.environ, QTNG_LIB_PATH=so, QTNG_REGTILE=rt)
+    for combo in sweep:
+        env = dict(os.environ, QTNG_LIB_PATH=so, **dict(combo))
         r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=300)
         line = (r.stdout.strip().splitlines() or [r.stderr[-300:]])[-1]
-        print(os.path.basename(so), "regtile=" + rt, line, flush=True)
+        print(os.path.basename(so), " ".join(f"{k}={v}" for k, v in combo), line, flush=True)
