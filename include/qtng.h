@@ -79,6 +79,10 @@ typedef struct qtng_plan_info {
   uint64_t n_fused_ops;      /* bucket ops evaluated inside segments */
   double dev_bytes;          /* HBM bytes the fused program must move: per
                                 unit, its materialised inputs + its output */
+  double fp64_ops;           /* FP64 multiplies + adds of the reference's
+                                NaiveBackend loop over all buckets */
+  double seg_fp64_ops;       /* ... of the buckets evaluated by seg_kernel */
+  double single_alg_bytes;   /* B_alg of the buckets run by level/outer kernels */
 } qtng_plan_info;
 
 /* ---------------------------------------------------------------- context */
@@ -192,6 +196,13 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
  * throughput measurement; n_runs back-to-back runs, total device time. */
 qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms);
 qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info);
+/* Host-only analysis of the fused-chain segments of the plan for all m
+ * edges.  Per segment (level-sorted): level, L (stages), rY, cY, nops; then
+ * per stage: nt, ns, main (-1 for stage 1), and per member: rank,
+ * initial (1 = gate / input-region tensor; a main placeholder has rank 0).
+ * *n_ints receives the size needed; nothing is written if cap is short. */
+qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged,
+                               int max_result_width, int* ints, int64_t cap, int64_t* n_ints);
 /* Host-only: the plan qtng_plan_create would build for all m edges (fuse=1:
  * fused-chain segments, fuse=0: one device op per bucket), without a device. */
 qtng_status qtng_plan_stats(int n, int m, const int* edges, int p, int merged,
@@ -199,6 +210,10 @@ qtng_status qtng_plan_stats(int n, int m, const int* edges, int p, int merged,
 /* Records of the last execution (edge_u/edge_v filled from the selection). */
 qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64_t cap,
                               int64_t* n_out);
+/* Device time of the last qtng_plan_execute summed per kernel kind (ms):
+ * ms3[0] level_kernel, ms3[1] outer_kernel, ms3[2] seg_kernel -- CUDA events
+ * on the stream each kernel runs on. */
+qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3);
 /* Per-level device time of the last qtng_plan_execute (ms), n_levels entries. */
 qtng_status qtng_plan_level_ms(const qtng_plan* plan, float* ms, int cap);
 void qtng_plan_destroy(qtng_plan* plan);

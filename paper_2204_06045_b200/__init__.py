@@ -417,6 +417,33 @@ def plan_stats(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfi
     return inf
 
 
+def plan_segments(g: Graph, p: int, merged: bool = False,
+                  cfg: Optional[EngineConfig] = None) -> List[dict]:
+    """Host-only description of the fused-chain segments of Plan(g, p):
+    level, L, ry, cy, nops, stages=[(nt, ns, main, [(rank, initial)])]."""
+    cfg = cfg or EngineConfig()
+    n_ints = C.c_int64(0)
+    probe = np.zeros(1, np.int32)
+    _check(lib.qtng_plan_segments(g.n, g.m, g.flat(), p, int(merged), cfg.max_result_width,
+                                  probe, 0, C.byref(n_ints)))
+    buf = np.zeros(max(1, n_ints.value), np.int32)
+    _check(lib.qtng_plan_segments(g.n, g.m, g.flat(), p, int(merged), cfg.max_result_width,
+                                  buf, len(buf), C.byref(n_ints)))
+    out, i = [], 0
+    while i < n_ints.value:
+        lv, L, ry, cy, nops = (int(x) for x in buf[i:i + 5])
+        i += 5
+        stages = []
+        for _ in range(L):
+            nt, ns, main = (int(x) for x in buf[i:i + 3])
+            i += 3
+            mem = [(int(buf[i + 2 * t]), int(buf[i + 2 * t + 1])) for t in range(nt)]
+            i += 2 * nt
+            stages.append((nt, ns, main, mem))
+        out.append(dict(level=lv, L=L, ry=ry, cy=cy, nops=nops, stages=stages))
+    return out
+
+
 def validate_energy(g: Graph, p: int, merged: bool = False,
                     cfg: Optional[EngineConfig] = None) -> None:
     """Host-only pre-flight of energy_expectation: raises the ScheduleError
@@ -536,6 +563,12 @@ class Plan:
         out = np.zeros(max(1, n), np.float32)
         _check(lib.qtng_plan_level_ms(self._h, out, n))
         return out[:n]
+
+    def kernel_ms(self) -> dict:
+        """Device ms of the last execute() per kernel kind (events on each kernel's stream)."""
+        ms = np.zeros(3, np.float32)
+        _check(lib.qtng_plan_kernel_ms(self._h, ms))
+        return {"level_kernel": float(ms[0]), "outer_kernel": float(ms[1]), "seg_kernel": float(ms[2])}
 
     def time_level(self, level: int = -1, n_runs: int = 10):
         lv, by, ms = C.c_int(0), C.c_double(0), C.c_float(0)

@@ -34,7 +34,9 @@ class PlanInfo(C.Structure):
                 ("alg_bytes", C.c_double), ("sum_ops", C.c_double),
                 ("arena_bytes", C.c_uint64), ("desc_bytes", C.c_uint64),
                 ("kernels_per_run", C.c_int32), ("n_segments", C.c_uint64),
-                ("n_fused_ops", C.c_uint64), ("dev_bytes", C.c_double)]
+                ("n_fused_ops", C.c_uint64), ("dev_bytes", C.c_double),
+                ("fp64_ops", C.c_double), ("seg_fp64_ops", C.c_double),
+                ("single_alg_bytes", C.c_double)]
 
 
 def _load():
@@ -76,10 +78,13 @@ def _load():
                                       C.POINTER(C.c_float)]
     lib.qtng_plan_run_device.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
     lib.qtng_plan_info_get.argtypes = [vp, C.POINTER(PlanInfo)]
+    lib.qtng_plan_segments.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int, i32p,
+                                       C.c_int64, C.POINTER(C.c_int64)]
     lib.qtng_plan_stats.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(PlanInfo)]
     lib.qtng_plan_records.argtypes = [vp, C.POINTER(Record), C.c_int64, C.POINTER(C.c_int64)]
     lib.qtng_plan_level_ms.argtypes = [vp, f32p, C.c_int]
+    lib.qtng_plan_kernel_ms.argtypes = [vp, f32p]
     lib.qtng_plan_destroy.argtypes = [vp]
     lib.qtng_plan_destroy.restype = None
     lib.qtng_plan_time_level.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_int),
@@ -94,6 +99,6 @@ EXPORTED = [
     "qtng_create", "qtng_destroy", "qtng_last_error", "qtng_version", "qtng_random_regular",
     "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
     "qtng_contract_schedule", "qtng_energy", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute",
-    "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_plan_records", "qtng_plan_level_ms",
+    "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_plan_segments", "qtng_plan_records", "qtng_plan_level_ms", "qtng_plan_kernel_ms",
     "qtng_plan_destroy", "qtng_plan_time_level",
 ]

@@ -240,26 +240,33 @@ struct DevProgram {
 
 // One level: the outer-join and segment kernels forked onto side streams, the
 // generic kernel on the main stream, joined before the next level.
+// kev (optional): 6 events bracketing this level's level / outer / segment
+// kernels on the streams they run on (per-kernel device time).
 void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const DevProgram& pr,
-                   double2* arena) {
+                   double2* arena, cudaEvent_t* kev = nullptr) {
   const bool fork2 = lv.outer_items > 0;
   const bool fork3 = lv.seg_items > 0 && (lv.items > 0 || fork2);
+  auto rec = [&](int k, cudaStream_t st) {
+    if (kev) QTNG_CUDA(cudaEventRecord(kev[k], st));
+  };
   if (fork2 || fork3) QTNG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
   if (fork2) {
     QTNG_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->fork_ev, 0));
+    rec(2, ctx->stream2);
     QTNG_CUDA(launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+    rec(3, ctx->stream2);
     QTNG_CUDA(cudaEventRecord(ctx->join_ev, ctx->stream2));
   }
-  if (fork3) {
-    QTNG_CUDA(cudaStreamWaitEvent(ctx->stream3, ctx->fork_ev, 0));
-    QTNG_CUDA(launch_segs(ctx->stream3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.segtab(), arena,
-                          pr.ctr(level), lv));
-    QTNG_CUDA(cudaEventRecord(ctx->join3_ev, ctx->stream3));
-  } else {
-    QTNG_CUDA(launch_segs(ctx->stream, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.segtab(), arena,
-                          pr.ctr(level), lv));
-  }
+  cudaStream_t s3 = fork3 ? ctx->stream3 : ctx->stream;
+  if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream3, ctx->fork_ev, 0));
+  rec(4, s3);
+  QTNG_CUDA(launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.segtab(), arena,
+                        pr.ctr(level), lv));
+  rec(5, s3);
+  if (fork3) QTNG_CUDA(cudaEventRecord(ctx->join3_ev, ctx->stream3));
+  rec(0, ctx->stream);
   QTNG_CUDA(launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+  rec(1, ctx->stream);
   if (fork2) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join3_ev, 0));
 }
@@ -278,11 +285,13 @@ void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* d
 // Enqueue the whole program on the context's stream: every level, then the
 // per-lightcone products.
 void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, double2* arena,
-                     std::vector<cudaEvent_t>* level_events) {
+                     std::vector<cudaEvent_t>* level_events,
+                     std::vector<cudaEvent_t>* kernel_events = nullptr) {
   cudaStream_t s = ctx->stream;
   for (size_t L = 0; L < hp.levels.size(); ++L) {
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
-    enqueue_level(ctx, hp.levels[L], L, pr, arena);
+    enqueue_level(ctx, hp.levels[L], L, pr, arena,
+                  kernel_events ? kernel_events->data() + 6 * L : nullptr);
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
   QTNG_CUDA(launch_final(s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
@@ -322,10 +331,13 @@ struct qtng_plan {
   PinBuf pin_gate, pin_terms;
   std::vector<cudaEvent_t> lev_ev;
   std::vector<float> level_ms;
+  std::vector<cudaEvent_t> ker_ev;  // 6 per level (enqueue_level)
+  float kernel_ms[3] = {0.f, 0.f, 0.f};  // level / outer / segment kernels, last execute
   cudaGraphExec_t graph = nullptr;
   uint64_t graph_gen = ~uint64_t{0};
   ~qtng_plan() {
     for (cudaEvent_t e : lev_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : ker_ev) cudaEventDestroy(e);
     if (graph) cudaGraphExecDestroy(graph);
   }
 };
@@ -640,6 +652,8 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
     plan->pin_terms.ensure(std::max<size_t>(1, cs.walks.size()) * sizeof(double2));
     plan->lev_ev.resize(hp.levels.size() + 1);
     for (cudaEvent_t& e : plan->lev_ev) QTNG_CUDA(cudaEventCreate(&e));
+    plan->ker_ev.resize(6 * hp.levels.size());
+    for (cudaEvent_t& e : plan->ker_ev) QTNG_CUDA(cudaEventCreate(&e));
     plan->level_ms.assign(hp.levels.size(), 0.f);
     *out = plan.release();
   });
@@ -676,6 +690,8 @@ qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* i
     plan->pin_terms.ensure(sizeof(double2));
     plan->lev_ev.resize(hp.levels.size() + 1);
     for (cudaEvent_t& e : plan->lev_ev) QTNG_CUDA(cudaEventCreate(&e));
+    plan->ker_ev.resize(6 * hp.levels.size());
+    for (cudaEvent_t& e : plan->ker_ev) QTNG_CUDA(cudaEventCreate(&e));
     plan->level_ms.assign(hp.levels.size(), 0.f);
     *out = plan.release();
   });
@@ -696,7 +712,7 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     QTNG_CUDA(cudaMemcpyAsync(ctx->A(), plan->pin_gate.p, hp.input_elems * sizeof(double2),
                               cudaMemcpyHostToDevice, ctx->stream));
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    enqueue_program(ctx, hp, plan->prog, ctx->A(), &plan->lev_ev);
+    enqueue_program(ctx, hp, plan->prog, ctx->A(), &plan->lev_ev, &plan->ker_ev);
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     const size_t nb = plan->edges.size() * sizeof(double2);
     QTNG_CUDA(cudaMemcpyAsync(plan->pin_terms.p, plan->prog.terms(), nb, cudaMemcpyDeviceToHost,
@@ -706,6 +722,17 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     QTNG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     for (size_t L = 0; L < hp.levels.size(); ++L)
       QTNG_CUDA(cudaEventElapsedTime(&plan->level_ms[L], plan->lev_ev[L], plan->lev_ev[L + 1]));
+    for (float& k : plan->kernel_ms) k = 0.f;
+    for (size_t L = 0; L < hp.levels.size(); ++L) {
+      const LevelLaunch& lv = hp.levels[L];
+      const uint32_t present[3] = {lv.items, lv.outer_items, lv.seg_items};
+      for (int k = 0; k < 3; ++k) {
+        if (!present[k]) continue;
+        float ms = 0.f;
+        QTNG_CUDA(cudaEventElapsedTime(&ms, plan->ker_ev[6 * L + 2 * k], plan->ker_ev[6 * L + 2 * k + 1]));
+        plan->kernel_ms[k] += ms;
+      }
+    }
     if (device_ms) *device_ms = ms;
     const double* t = static_cast<const double*>(plan->pin_terms.p);
     if (terms) std::memcpy(terms, t, nb);
@@ -758,6 +785,9 @@ void fill_info(const HostPlan& hp, int n_lightcones, qtng_plan_info* info) {
     info->n_segments = hp.segs.size();
     info->n_fused_ops = hp.n_fused_ops;
     info->dev_bytes = hp.dev_bytes;
+    info->fp64_ops = hp.fp64_ops;
+    info->seg_fp64_ops = hp.seg_fp64_ops;
+    info->single_alg_bytes = hp.single_alg_bytes;
 }
 }  // namespace
 
@@ -765,6 +795,38 @@ qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info) {
   return guarded([&] {
     if (!plan || !info) throw Error(kInvalidInput, "null argument");
     fill_info(plan->hp, static_cast<int>(plan->edges.size()), info);
+  });
+}
+
+qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged,
+                               int max_result_width, int* ints, int64_t cap, int64_t* n_ints) {
+  return guarded([&] {
+    if (p < 1) throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+    const Graph g = graph_from(n, m, edges);
+    const ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, selection(m, m, nullptr));
+    std::vector<const WalkResult*> ptrs;
+    for (const WalkResult& w : cs.walks) {
+      if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
+      ptrs.push_back(&w);
+    }
+    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, true);
+    std::vector<int> out;
+    for (size_t L = 0; L < hp.levels.size(); ++L)
+      for (uint32_t k = 0; k < hp.levels[L].seg_count; ++k) {
+        const DevSeg& sg = hp.segs[hp.levels[L].seg_begin + k];
+        out.insert(out.end(), {static_cast<int>(L), sg.nst, sg.ry, sg.cy, sg.nops});
+        for (int i = 0; i < sg.nst; ++i) {
+          const DevStage& st = hp.stages[sg.stage + i];
+          out.insert(out.end(), {st.nt, st.ns, st.main == kSegMain ? -1 : st.main});
+          for (int t = 0; t < st.nt; ++t) {
+            const DevTensor& x = hp.trefs[sg.tref + st.op0 + t];
+            out.push_back(x.rank);
+            out.push_back(x.rank && x.off < hp.input_elems ? 1 : 0);
+          }
+        }
+      }
+    *n_ints = static_cast<int64_t>(out.size());
+    if (static_cast<int64_t>(out.size()) <= cap) std::copy(out.begin(), out.end(), ints);
   });
 }
 
@@ -808,6 +870,13 @@ qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64
         r.elapsed_s = std::max(1e-9, 1e-3 * plan->level_ms[L] * share);
         r.flops_est = 8.0 * static_cast<double>(r.ops) / r.elapsed_s;
       }
+  });
+}
+
+qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3) {
+  return guarded([&] {
+    if (!plan || !ms3) throw Error(kInvalidInput, "null argument");
+    for (int k = 0; k < 3; ++k) ms3[k] = plan->kernel_ms[k];
   });
 }
 

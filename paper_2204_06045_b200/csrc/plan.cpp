@@ -5,6 +5,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "pool.hpp"
@@ -459,6 +460,13 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       const Op& o = op_at(g);
       hp.level_bytes[L] += op_bytes[g];
       hp.alg_bytes += op_bytes[g];
+      // the reference's FP64 operations (NaiveBackend::contract): per summed
+      // assignment nt-1 complex products (4 mul + 2 add/sub), per output
+      // 2^ns - 1 complex additions
+      const double fl = 6.0 * std::ldexp(1.0, o.width) * (o.nin - 1) +
+                        2.0 * std::ldexp(1.0, o.r) * (std::ldexp(1.0, o.ns) - 1.0);
+      hp.fp64_ops += fl;
+      if (unit_len[u] > 1) hp.seg_fp64_ops += fl; else hp.single_alg_bytes += op_bytes[g];
       if (o.bucket_seq >= 0) {
         hp.sum_ops += static_cast<double>(uint64_t{1} << o.width);
         ++hp.n_buckets;

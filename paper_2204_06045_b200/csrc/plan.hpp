@@ -25,6 +25,9 @@ struct HostPlan {
   // per unit sum of its materialised inputs + its output
   double dev_bytes = 0;
   uint64_t n_fused_ops = 0;            // ops evaluated inside segments
+  double fp64_ops = 0;                 // the reference's FP64 mul/add count (all ops)
+  double seg_fp64_ops = 0;             // ... of the ops inside segments
+  double single_alg_bytes = 0;         // B_alg of the single (level/outer kernel) ops
   std::vector<uint64_t> scalar_off;    // per lightcone: its scalar results, production order
   std::vector<uint32_t> lc_begin;      // n_lightcones + 1 prefix into scalar_off
   uint64_t input_elems = 0;

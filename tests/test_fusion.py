@@ -1,0 +1,105 @@
+"""Fused bucket chains (device_plan.hpp "segments").
+
+CPU: the planner's segment formation is a pure regrouping -- same buckets,
+same records, same reference accounting -- with the HBM traffic of the fused
+program far below the reference's per-bucket bytes, and every fused stage of
+the shape the seg_kernel evaluates (main member last, one summed var).
+
+GPU: the fused program is bit-identical to the one-op-per-bucket program and
+to the reference at every segment length (QTNG_SEG_J) -- each intermediate
+element is produced by the same operation sequence whether it lives in HBM
+or in a register.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _cfg(golden, name):
+    c = golden["configs"][name]
+    return c, len(c["gammas"])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
+def test_fusion_is_a_regrouping(q, golden, name):
+    c, p = _cfg(golden, name)
+    g = q.random_regular(c["n"], 3, c["seed"])
+    fused, plain = q.plan_stats(g, p, fuse=True), q.plan_stats(g, p, fuse=False)
+    assert fused.n_buckets == plain.n_buckets
+    assert fused.alg_bytes == plain.alg_bytes and fused.sum_ops == plain.sum_ops
+    assert fused.max_width == plain.max_width == max(max(q.simulate_widths(g, i, p))
+                                                     for i in range(g.m))
+    assert plain.n_segments == 0 and plain.dev_bytes == plain.alg_bytes
+    assert fused.n_segments > 0
+    # every bucket is either one device op or one stage of a segment
+    assert fused.n_device_ops + fused.n_fused_ops == plain.n_device_ops
+    assert fused.n_levels < plain.n_levels
+    assert fused.dev_bytes < plain.dev_bytes
+    assert fused.arena_bytes <= plain.arena_bytes
+
+
+def test_c2_fused_traffic(q, golden):
+    c, p = _cfg(golden, "C2")
+    g = q.random_regular(c["n"], 3, c["seed"])
+    inf = q.plan_stats(g, p)
+    # 19.8 GB of per-bucket bytes -> about 1 GB the fused program must move
+    assert inf.alg_bytes == pytest.approx(1.977e10, rel=1e-3)
+    assert inf.dev_bytes < 0.08 * inf.alg_bytes
+
+
+def test_segment_shapes(q, golden):
+    c, p = _cfg(golden, "C2")
+    g = q.random_regular(c["n"], 3, c["seed"])
+    segs = q.plan_segments(g, p)
+    assert segs and len(segs) == q.plan_stats(g, p).n_segments
+    levels = [s["level"] for s in segs]
+    assert levels == sorted(levels)
+    for s in segs:
+        assert 2 <= s["L"] <= 9 and s["cy"] == min(s["ry"], 5)
+        assert s["nops"] == sum(st[0] for st in s["stages"]) <= 16
+        nt1, ns1, main1, _ = s["stages"][0]
+        assert main1 == -1 and ns1 <= 1 and nt1 <= 6
+        for nt, ns, main, mem in s["stages"][1:]:
+            assert ns == 1 and nt <= 4 and main == nt - 1
+            assert mem[main][0] == 0  # placeholder: read from registers
+            assert all(rank > 0 for rank, _ in mem[:main])
+        # stage i's result rank shrinks by its summed var: rY = r_1 - (L - 1)
+
+
+def _child_energy(name, env):
+    code = r'''
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2204_06045_b200 as q
+c = json.load(open(%r))["configs"][%r]
+g = q.random_regular(c["n"], 3, c["seed"])
+plan = q.Plan(g, len(c["gammas"]))
+t = plan.execute(q.Angles(c["gammas"], c["betas"]))
+inf = plan.info()
+print(json.dumps({"terms": [[float(x.real), float(x.imag)] for x in t], "segments": int(inf.n_segments)}))
+''' % (ROOT, os.path.join(ROOT, "tests", "golden", "energies.json"), name)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_fused_equals_unfused_bitwise(golden, name):
+    ref = np.array([complex(x, y) for x, y in golden["configs"][name]["terms_naive"]])
+    plain = _child_energy(name, {"QTNG_FUSE": "0"})
+    assert plain["segments"] == 0
+    for j in ("1", "3", "8"):
+        fused = _child_energy(name, {"QTNG_SEG_J": j})
+        assert fused["segments"] > 0
+        assert fused["terms"] == plain["terms"], f"QTNG_SEG_J={j}"
+    got = np.array([complex(x, y) for x, y in plain["terms"]])
+    assert np.array_equal(got, ref)

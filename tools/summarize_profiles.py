@@ -50,20 +50,25 @@ def launches(src, dst_dir):
     tot_t = sum(d[i]["gpu__time_duration.sum"] for i in half)
     tot_b = sum(d[i].get("dram__bytes_read.sum", 0) + d[i].get("dram__bytes_write.sum", 0)
                 for i in half)
-    lvl_b = sum(d[i].get("dram__bytes_read.sum", 0) + d[i].get("dram__bytes_write.sum", 0)
-                for i in half if names[i].startswith("level_kernel"))
-    lvl_t = sum(d[i]["gpu__time_duration.sum"] for i in half if names[i].startswith("level_kernel"))
+    kinds = defaultdict(lambda: [0.0, 0.0])  # kernel -> [ns, DRAM bytes] per step
+    for i in half:
+        k = kinds[names[i].split("<")[0]]
+        k[0] += d[i]["gpu__time_duration.sum"]
+        k[1] += d[i].get("dram__bytes_read.sum", 0) + d[i].get("dram__bytes_write.sum", 0)
     lines = [f"launches per step: {len(half)}; step total {tot_t / 1e3:.1f} us (ncu-serialised); "
-             f"DRAM {tot_b / 1e9:.3f} GB; level_kernel share {100 * lvl_t / tot_t:.1f}% of time",
+             f"DRAM {tot_b / 1e9:.3f} GB; " + "; ".join(
+                 f"{k} {100 * v[0] / tot_t:.1f}% of time, {v[1] / 1e9:.3f} GB"
+                 for k, v in sorted(kinds.items(), key=lambda kv: -kv[1][0])),
              "idx kernel us DRAM_MB GB/s share%"]
     for j, i in enumerate(half):
         t = d[i]["gpu__time_duration.sum"]
         b = d[i].get("dram__bytes_read.sum", 0) + d[i].get("dram__bytes_write.sum", 0)
         lines.append(f"{j} {names[i]} {t / 1e3:.1f} {b / 1e6:.1f} {b / t:.0f} {100 * t / tot_t:.2f}")
     open(os.path.join(dst_dir, "launch_summary.txt"), "w").write("\n".join(lines) + "\n")
-    json.dump({"level_kernel_dram_bytes_per_step": lvl_b, "level_kernel_ncu_us_per_step": lvl_t / 1e3,
+    json.dump({"dram_bytes_per_step": {k: v[1] for k, v in kinds.items()},
+               "ncu_us_per_step": {k: v[0] / 1e3 for k, v in kinds.items()},
                "source": os.path.relpath(os.path.join(dst_dir, "launches.csv"), ROOT)},
-              open(os.path.join(dst_dir, "traffic.json"), "w"))
+              open(os.path.join(dst_dir, "traffic.json"), "w"), indent=1)
     return lines[0]
 
 
@@ -91,13 +96,18 @@ def main():
     src = os.path.join(ROOT, "gpurun_out", tag)
     dst = os.path.join(ROOT, "profiles", tag)
     os.makedirs(dst, exist_ok=True)
-    for f in ("bench.json", "microbench.txt", "pytest_gpu.txt", "smoke.txt", "launches.csv", "host.txt"):
+    for f in ("bench.json", "bench_reference.json", "microbench.txt", "pytest_gpu.txt", "smoke.txt",
+              "launches.csv", "host.txt", "levels.txt"):
         if os.path.exists(os.path.join(src, f)):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
     if os.path.exists(os.path.join(src, "launches.csv")):
         print(launches(os.path.join(src, "launches.csv"), dst))
     if os.path.exists(os.path.join(src, "prof_big.ncu-rep")):
         full_capture(os.path.join(src, "prof_big.ncu-rep"), os.path.join(dst, "ncu_widest_level.txt"))
+    if os.path.exists(os.path.join(src, "seg.ncu-rep")):
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"),
+                              os.path.join(src, "seg.ncu-rep"), "30"], capture_output=True, text=True).stdout
+        open(os.path.join(dst, "ncu_seg_kernel.txt"), "w").write(out)
     print("wrote", dst)
 
 
