@@ -479,7 +479,7 @@ qtng_status qtng_plan_dump(int n, int m, const int* edges, int p, int merged,
       ptrs.push_back(&w);
     }
     // every op as its own device op (no chain fusion): the op-class view
-    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, false);
+    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, false, true);
     std::vector<int> out;
     for (size_t L = 0; L < hp.levels.size(); ++L)
       for (uint32_t k = 0; k < hp.levels[L].op_count + hp.levels[L].outer_count; ++k) {
@@ -639,7 +639,7 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
     plan->edges = cs.edges;
     std::vector<const WalkResult*> ptrs;
     for (const WalkResult& w : cs.walks) ptrs.push_back(&w);
-    plan->hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems);
+    plan->hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
     const HostPlan& hp = plan->hp;
     const DescLayout L = layout_of(hp);
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -809,7 +809,7 @@ qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged
       if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
       ptrs.push_back(&w);
     }
-    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, true);
+    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, true, true);
     std::vector<int> out;
     for (size_t L = 0; L < hp.levels.size(); ++L)
       for (uint32_t k = 0; k < hp.levels[L].seg_count; ++k) {
@@ -845,7 +845,7 @@ qtng_status qtng_plan_stats(int n, int m, const int* edges, int p, int merged,
       ptrs.push_back(&cs.walks[i]);
     }
     const HostPlan hp =
-        build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse != 0);
+        build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse != 0, true);
     fill_info(hp, static_cast<int>(ptrs.size()), info);
   });
 }
@@ -950,7 +950,7 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
     }
     std::vector<double> t(2 * cs.walks.size(), 0.0);
     if (!ok.empty()) {
-      const HostPlan hp = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems);
+      const HostPlan hp = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
       std::vector<double> table(2 * hp.input_elems);
       fill_gate_table(p, gammas, betas, table.data());
       std::vector<double2> tt(ok.size());

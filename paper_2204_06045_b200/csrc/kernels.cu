@@ -432,6 +432,7 @@ __global__ void seg_prep_kernel(const DevSeg* __restrict__ segs, uint32_t n_segs
     }
     if (lane == 0) {
       t.sd = s;
+      t.kind = d->kind;
       t.off = d->off;
     }
   }
@@ -444,20 +445,43 @@ struct ChainWarp {
   double2 acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
 };
 
+// (r, 0) * y and p * (r, 0): equal to cmul up to the sign of an exact zero.
+__device__ __forceinline__ double2 rscale(double r, double2 y) {
+  return make_double2(__dmul_rn(r, y.x), __dmul_rn(r, y.y));
+}
+
+// One left-fold step p * y where either factor may be a real scalar (r, 0).
+__device__ __forceinline__ double2 fmul(double2 p, bool p_real, double2 y, bool y_real) {
+  if (y_real) return rscale(y.x, p);
+  if (p_real) return rscale(p.x, y);
+  return cmul(p, y);
+}
+
 // Side-member product P_i (left fold of members [op0, op0+m)) at digit
-// assignment j; m >= 1.
+// assignment j; m >= 1.  *real: P is a real scalar (r, 0).
 __device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                               const double2* __restrict__ arena, int op0, int m,
-                                              uint32_t j, int lane) {
+                                              uint32_t j, int lane, bool* real) {
   const uint32_t jl = j & 15u, jh = j >> 4;
   double2 p = make_double2(0.0, 0.0);
+  bool pr = false;
   for (int t = 0; t < m; ++t) {
     const int op = op0 + t;
     const SegOpTab* tb = tab + op;
-    const double2 x = ld(arena + __ldg(&tb->off) +
-                         (cw.toff[op] + __ldg(&tb->llane[lane]) + __ldg(&tb->dlo[jl]) + __ldg(&tb->dhi[jh])));
-    p = t == 0 ? x : cmul(p, x);
+    const bool xr = __ldg(&tb->kind) == kTensorRealScalar;
+    const double2 x = xr ? make_double2(__ldg(&(arena + __ldg(&tb->off))->x), 0.0)
+                         : ld(arena + __ldg(&tb->off) +
+                              (cw.toff[op] + __ldg(&tb->llane[lane]) + __ldg(&tb->dlo[jl]) +
+                               __ldg(&tb->dhi[jh])));
+    if (t == 0) {
+      p = x;
+      pr = xr;
+    } else {
+      p = fmul(p, pr, x, xr);
+      pr = false;
+    }
   }
+  *real = pr;
   return p;
 }
 
@@ -466,13 +490,16 @@ __device__ __forceinline__ double2 chain_term(const ChainWarp& cw, const SegOpTa
                                               const double2* __restrict__ arena, const DevStage st,
                                               uint32_t j, double2 v, int lane) {
   const int m = st.nt - 1;
-  return m ? cmul(chain_side(cw, tab, arena, st.op0, m, j, lane), v) : v;
+  if (!m) return v;
+  bool real;
+  const double2 p = chain_side(cw, tab, arena, st.op0, m, j, lane, &real);
+  return real ? rscale(p.x, v) : cmul(p, v);
 }
 
 // One tile: 2^J stage-1 evaluations (NT members, NS summed bits), in groups
 // of 2^U consecutive j (stages 2..U+1 resolved in registers, four independent
 // stage-1 products in flight), then the climb above each group.
-template <int NT, int NS, int U>
+template <int NT, int NS, int U, int K0>
 __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                            const DevSeg& sg, double2* __restrict__ arena,
                                            uint32_t tile, int lane) {
@@ -481,6 +508,9 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
   const uint32_t nj = 1u << (L - 1);
   const double2* B[NT];
   uint32_t o[NT], sdl[NT], d0[NT], d1[NT];
+  // K0: member 0 is a real scalar r (the |+> state on the summed var): the
+  // first product (r, 0) * M1 becomes a scale, and member 0 is not gathered
+  const double r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : 0.0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     B[t] = arena + __ldg(&tab[t].off);
@@ -503,13 +533,13 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
       uint32_t oq[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t) oq[t] = o[t] + ((q & 1) ? d0[t] : 0u) + ((q & 2) ? d1[t] : 0u);
-      double2 x = ld(B[0] + oq[0]);
+      double2 x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
 #pragma unroll
-      for (int t = 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
+      for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
       if (NS) {
-        double2 p = ld(B[0] + oq[0] + sdl[0]);
+        double2 p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
 #pragma unroll
-        for (int t = 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
+        for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
         x = cadd(x, p);
       }
       v[q] = x;
@@ -542,8 +572,14 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
                                              const DevSeg& sg, double2* __restrict__ arena,
                                              uint32_t tile, int lane) {
   // wide heads use pairs of j (register pressure), the rest groups of four
-  if (NT <= 4 && sg.nst >= 3) chain_tile<NT, NS, (NT <= 4 ? 2 : 1)>(cw, tab, sg, arena, tile, lane);
-  else chain_tile<NT, NS, 1>(cw, tab, sg, arena, tile, lane);
+  const bool k0 = NT >= 2 && __ldg(&tab[0].kind) == kTensorRealScalar;
+  if (NT <= 4 && sg.nst >= 3) {
+    if (k0) chain_tile<NT, NS, (NT <= 4 ? 2 : 1), (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+    else chain_tile<NT, NS, (NT <= 4 ? 2 : 1), 0>(cw, tab, sg, arena, tile, lane);
+  } else {
+    if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+    else chain_tile<NT, NS, 1, 0>(cw, tab, sg, arena, tile, lane);
+  }
 }
 
 #ifndef QTNG_SEG_MINB

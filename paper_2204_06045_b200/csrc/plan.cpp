@@ -88,7 +88,8 @@ bool fuse_default() {
   return on;
 }
 
-HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems, bool fuse) {
+HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems, bool fuse,
+                    bool qaoa_gates) {
   HostPlan hp;
   hp.input_elems = input_elems;
   const int C = static_cast<int>(cones.size());
@@ -430,6 +431,8 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
           x.off = in.initial ? static_cast<uint64_t>(in.ref) : out[cb0 + in.ref];
           if (x.off == kNoOut) { chunk_err[ch] = 3; return; }
           x.rank = static_cast<uint8_t>(in.rank);
+          if (qaoa_gates && in.initial && in.rank == 1 && in.ref == kSlotPlus * kSlotElems)
+            x.kind = kTensorRealScalar;
           const int32_t* iv = w.in_vars(in);
           for (int ax = 0; ax < in.rank; ++ax) {
             if (pm_stamp[iv[ax]] != stamp) { chunk_err[ch] = 2; return; }

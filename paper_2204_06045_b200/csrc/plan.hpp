@@ -53,7 +53,9 @@ bool fuse_default();
 // whose first `input_elems` elements hold the inputs.  Chains of buckets whose
 // intermediate spans the consumer's whole width become fused segments;
 // fuse=false keeps every op a separate level-kernel op (no chain fusion).
+// qaoa_gates: the input region is the QAOA gate table (fill_gate_table), so
+// initial operands are classified by gate slot (DevTensor::kind).
 HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems,
-                    bool fuse = fuse_default());
+                    bool fuse = fuse_default(), bool qaoa_gates = false);
 
 }  // namespace qtng
