@@ -465,7 +465,9 @@ __device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const SegOpTa
   const uint32_t jl = j & 15u, jh = j >> 4;
   double2 p = make_double2(0.0, 0.0);
   bool pr = false;
-  for (int t = 0; t < m; ++t) {
+#pragma unroll
+  for (int t = 0; t < kSegMaxNt - 1; ++t) {  // unrolled: loads of independent terms overlap
+    if (t >= m) break;
     const int op = op0 + t;
     const SegOpTab* tb = tab + op;
     const bool xr = __ldg(&tb->kind) == kTensorRealScalar;

@@ -9,10 +9,17 @@ sys.path.insert(0, %r)
 import paper_2204_06045_b200 as q
 g = q.random_regular(30, 3, 104478); a = q.Angles([0.30,0.25,0.20,0.15],[0.35,0.30,0.25,0.20])
 ctx = q.Context(0); plan = q.Plan(g, 4, ctx=ctx)
-t = plan.execute(a); e = 0.5*g.m - 0.5*float(np.sum(t.real))
+try:
+    t = plan.execute(a); e = 0.5*g.m - 0.5*float(np.sum(t.real))
+except Exception as ex:  # timing experiments may compute garbage
+    e = repr(ex)[:60]
 for _ in range(3): plan.run_device(1)
 ms = plan.run_device(20) / 20
-plan.execute(a); lv = plan.level_ms()
+try:
+    plan.execute(a)
+except Exception:
+    pass
+lv = plan.level_ms()
 L, by, lms = plan.time_level(-1, 20)
 print(json.dumps(dict(ms_step=ms, level_sum=float(lv.sum()), big_level=L, big_gbs=by/lms/1e6, energy=e,
                       top=[round(float(x),1) for x in sorted(lv*1e3)[-6:]])))
