@@ -260,7 +260,7 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
   cudaStream_t s3 = fork3 ? ctx->stream3 : ctx->stream;
   if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream3, ctx->fork_ev, 0));
   rec(4, s3);
-  QTNG_CUDA(launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.segtab(), arena,
+  QTNG_CUDA(launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(), pr.segtab(), arena,
                         pr.ctr(level), lv));
   rec(5, s3);
   if (fork3) QTNG_CUDA(cudaEventRecord(ctx->join3_ev, ctx->stream3));

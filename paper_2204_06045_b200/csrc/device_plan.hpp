@@ -79,7 +79,7 @@ static_assert(sizeof(DevTensor) == 48, "DevTensor layout");
 //   32..63   tile-number bit (code - 32 = Y bit - cY)
 //   64       stage 1's own summed bit (stage 1 sums at most one var)
 constexpr int kSegYBits = 5;         // cY = min(rY, kSegYBits)
-constexpr int kSegMaxJ = 8;          // digits per segment (dlo/dhi tables: 2 x 4 bits)
+constexpr int kSegMaxJ = 6;          // digits per segment (dlo/dhi tables: 4 + 2 bits)
 constexpr int kSegMaxStages = kSegMaxJ + 1;
 constexpr int kSegMaxOps = 16;       // operands per segment (all stages)
 constexpr int kSegMaxNt1 = 6;        // members of stage 1
@@ -115,15 +115,23 @@ struct alignas(16) SegOpTab {
   uint32_t dtile[32];          // offset per tile-number bit
   uint32_t llane[32];          // lane part of the offset, per lane
 };
-static_assert(sizeof(SegOpTab) == 464, "SegOpTab layout");
+static_assert(sizeof(SegOpTab) % 16 == 0, "SegOpTab layout");
 
 struct DevStage {
   uint8_t nt;    // members (bucket member order)
   uint8_t main;  // position of the main member (kSegMain for stage 1)
   uint8_t ns;    // summed bits of the stage (0 or 1)
   uint8_t op0;   // index of member 0 among the segment's DevTensors
+  // Fused stage whose side members are all input-region tensors of rank <= 2
+  // over s_i and at most two more vars u[0], u[1] (codes as DevTensor::src,
+  // kNoVar if absent): the side product P_i depends only on (s_i, u) and is
+  // tabulated once per tile instead of gathered per term.
+  uint8_t ptab;  // 1 = tabulated
+  uint8_t u[2];
+  uint8_t pad;
 };
-static_assert(sizeof(DevStage) == 4, "DevStage layout");
+static_assert(sizeof(DevStage) == 8, "DevStage layout");
+constexpr uint8_t kNoVar = 0xff;
 
 // One level of the level-synchronous schedule: generic ops
 // [op_begin, op_begin+op_count) of the level-sorted op array (`items` warp

@@ -442,6 +442,8 @@ __global__ void seg_prep_kernel(const DevSeg* __restrict__ segs, uint32_t n_segs
 struct ChainWarp {
   uint32_t toff[kSegMaxOps];             // tile part of each operand's offset
   DevStage st[kSegMaxStages];
+  double2 ptab[kSegMaxStages][8];        // tabulated side products P_i(s_i, u0, u1) of this tile
+  uint8_t preal[kSegMaxStages];          // 1: P_i is a real scalar (scale instead of multiply)
   double2 acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
 };
 
@@ -487,10 +489,31 @@ __device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const SegOpTa
   return p;
 }
 
-// term of stage i (DevStage st) at digit assignment j: P_i(j) * v, or v.
+#ifndef QTNG_SEG_PTAB
+#define QTNG_SEG_PTAB 1  // tabulated side products in the climb
+#endif
+#ifndef QTNG_SEG_U2_MAXNT
+#define QTNG_SEG_U2_MAXNT 0  // widest head evaluated in groups of four j (tuned: pairs everywhere)
+#endif
+
+// Index bit of a tabulated side product from var code c (lane / digit bit;
+// tile bits are fixed per tile and folded into the table).
+__device__ __forceinline__ uint32_t ptab_bit(uint8_t c, uint32_t j, int lane) {
+  if (c < kLaneSrcEnd) return (static_cast<uint32_t>(lane) >> c) & 1u;
+  if (c >= kJSrc && c < kTileSrc) return (j >> (c - kJSrc)) & 1u;
+  return 0u;
+}
+
+// term of stage i = k + 2 (DevStage st) at digit assignment j: P_i(j) * v, or v.
 __device__ __forceinline__ double2 chain_term(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                               const double2* __restrict__ arena, const DevStage st,
-                                              uint32_t j, double2 v, int lane) {
+                                              int k, uint32_t j, double2 v, int lane) {
+  if (QTNG_SEG_PTAB && st.ptab) {
+    const uint32_t idx = ((j >> k) & 1u) | (ptab_bit(st.u[0], j, lane) << 1) |
+                         (ptab_bit(st.u[1], j, lane) << 2);
+    const double2 p = cw.ptab[k + 1][idx];
+    return cw.preal[k + 1] ? rscale(p.x, v) : cmul(p, v);
+  }
   const int m = st.nt - 1;
   if (!m) return v;
   bool real;
@@ -547,17 +570,19 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
       v[q] = x;
     }
     // stage 2 over bit 0, stage 3 over bit 1 (U == 2)
-    double2 x = cadd(chain_term(cw, tab, arena, st2, j, v[0], lane), chain_term(cw, tab, arena, st2, j | 1u, v[1], lane));
+    double2 x = cadd(chain_term(cw, tab, arena, st2, 0, j, v[0], lane),
+                     chain_term(cw, tab, arena, st2, 0, j | 1u, v[1], lane));
     if (U > 1) {
-      const double2 y = cadd(chain_term(cw, tab, arena, st2, j | 2u, v[2], lane),
-                             chain_term(cw, tab, arena, st2, j | 3u, v[3], lane));
-      x = cadd(chain_term(cw, tab, arena, st3, j, x, lane), chain_term(cw, tab, arena, st3, j | 2u, y, lane));
+      const double2 y = cadd(chain_term(cw, tab, arena, st2, 0, j | 2u, v[2], lane),
+                             chain_term(cw, tab, arena, st2, 0, j | 3u, v[3], lane));
+      x = cadd(chain_term(cw, tab, arena, st3, 1, j, x, lane),
+               chain_term(cw, tab, arena, st3, 1, j | 2u, y, lane));
     }
     // climb: stage i = k + 2 >= U + 2 while the carry propagates
     const uint32_t jj = j | (G - 1);
     bool carry = true;
     for (int k = U; k + 2 <= L; ++k) {
-      const double2 term = chain_term(cw, tab, arena, cw.st[k + 1], jj, x, lane);
+      const double2 term = chain_term(cw, tab, arena, cw.st[k + 1], k, jj, x, lane);
       if (!((jj >> k) & 1u)) {
         cw.acc[k - 1][lane] = term;
         carry = false;
@@ -575,12 +600,54 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
                                              uint32_t tile, int lane) {
   // wide heads use pairs of j (register pressure), the rest groups of four
   const bool k0 = NT >= 2 && __ldg(&tab[0].kind) == kTensorRealScalar;
-  if (NT <= 4 && sg.nst >= 3) {
-    if (k0) chain_tile<NT, NS, (NT <= 4 ? 2 : 1), (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
-    else chain_tile<NT, NS, (NT <= 4 ? 2 : 1), 0>(cw, tab, sg, arena, tile, lane);
+  constexpr int U = NT <= QTNG_SEG_U2_MAXNT ? 2 : 1;
+  if (U == 2 && sg.nst >= 3) {
+    if (k0) chain_tile<NT, NS, U, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+    else chain_tile<NT, NS, U, 0>(cw, tab, sg, arena, tile, lane);
   } else {
     if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
     else chain_tile<NT, NS, 1, 0>(cw, tab, sg, arena, tile, lane);
+  }
+}
+
+// Tabulate the side products of the fused stages for this tile: lane
+// (stage, entry) folds the stage's side members at (s_i, u0, u1) = entry bits
+// (a tile-bit u takes this tile's value) exactly like chain_side.  Cold path:
+// kept out of line so the hot loop's registers are not spilled for it.
+__device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
+                                              const DevTensor* __restrict__ trefs,
+                                              const double2* __restrict__ arena, uint32_t tile,
+                                              int lane) {
+  for (int base = 8; base < 8 * sg.nst; base += 32) {
+    const int i = (base + lane) >> 3, e = (base + lane) & 7;
+    if (i < sg.nst && cw.st[i].ptab) {
+      const DevStage st = cw.st[i];
+      const uint8_t own = static_cast<uint8_t>(kJSrc + (i - 1));
+      auto val = [&](uint8_t c) -> uint32_t {
+        if (c == own) return e & 1;
+        const int w = c == st.u[0] ? 0 : 1;
+        if (c >= kTileSrc && c < kSumSrc) return (tile >> (c - kTileSrc)) & 1u;
+        return (e >> (1 + w)) & 1;
+      };
+      double2 p = make_double2(0.0, 0.0);
+      bool pr = false;
+      for (int t = 0; t < st.nt - 1; ++t) {
+        const DevTensor* d = trefs + sg.tref + st.op0 + t;
+        const int rank = d->rank;
+        uint32_t o = 0;
+        for (int ax = 0; ax < rank; ++ax) o |= val(d->src[ax]) << (rank - 1 - ax);
+        const bool xr = d->kind == kTensorRealScalar;
+        const double2 x = xr ? make_double2(__ldg(&(arena + d->off)->x), 0.0) : ld(arena + d->off + o);
+        if (t == 0) {
+          p = x;
+          pr = xr;
+        } else {
+          p = fmul(p, pr, x, xr);
+          pr = false;
+        }
+      }
+      cw.ptab[i][e] = p;
+    }
   }
 }
 
@@ -589,8 +656,9 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
 #endif
 __global__ void __launch_bounds__(32, QTNG_SEG_MINB)
 seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
-           const DevStage* __restrict__ stages, const SegOpTab* __restrict__ segtab,
-           double2* __restrict__ arena, uint32_t seg_count, uint32_t items, uint32_t* ctr) {
+           const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
+           const SegOpTab* __restrict__ segtab, double2* __restrict__ arena, uint32_t seg_count,
+           uint32_t items, uint32_t* ctr) {
   __shared__ ChainWarp cw;
   const int lane = threadIdx.x;
   // dynamic tile queue (segments are sorted by per-tile cost, largest first);
@@ -613,7 +681,14 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
         cur = static_cast<int>(lo);
         sg = segs[lo];
         __syncwarp();
-        if (lane < sg.nst) cw.st[lane] = stages[sg.stage + lane];
+        if (lane < sg.nst) {
+          const DevStage st = stages[sg.stage + lane];
+          cw.st[lane] = st;
+          bool real = lane > 0 && st.nt > 1;  // every side member a real scalar
+          for (int t = 0; real && t < st.nt - 1; ++t)
+            real = __ldg(&segtab[sg.tref + st.op0 + t].kind) == kTensorRealScalar;
+          cw.preal[lane] = real ? 1 : 0;
+        }
       }
       cur_begin = __ldg(ibeg + lo);
       cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
@@ -625,6 +700,7 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
       const uint32_t sum = __reduce_add_sync(kFull, v);
       if (lane == 0) cw.toff[op] = sum;
     }
+    chain_ptab_build(cw, sg, trefs, arena, tile, lane);
     __syncwarp();
     const DevStage s1 = cw.st[0];
     switch (s1.nt * 2 + s1.ns) {
@@ -727,11 +803,11 @@ cudaError_t launch_seg_prep(cudaStream_t s, const DevSeg* segs, uint32_t n_segs,
 }
 
 cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
-                        const DevStage* stages, const SegOpTab* segtab, double2* arena,
-                        uint32_t* ctr, const LevelLaunch& lv) {
+                        const DevStage* stages, const DevTensor* trefs, const SegOpTab* segtab,
+                        double2* arena, uint32_t* ctr, const LevelLaunch& lv) {
   if (lv.seg_items == 0) return cudaSuccess;
   seg_kernel<<<seg_grid(lv.seg_items), 32, 0, s>>>(
-      segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, segtab, arena, lv.seg_count,
+      segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, trefs, segtab, arena, lv.seg_count,
       lv.seg_items, ctr);
   return cudaGetLastError();
 }

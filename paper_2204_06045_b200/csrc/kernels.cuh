@@ -22,8 +22,8 @@ cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
 
 // The level's fused-chain segments (seg_kernel), concurrent with the others.
 cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
-                        const DevStage* stages, const SegOpTab* segtab, double2* arena,
-                        uint32_t* ctr, const LevelLaunch& lv);
+                        const DevStage* stages, const DevTensor* trefs, const SegOpTab* segtab,
+                        double2* arena, uint32_t* ctr, const LevelLaunch& lv);
 
 // Build the segments' SegOpTab entries (once per descriptor upload).
 cudaError_t launch_seg_prep(cudaStream_t s, const DevSeg* segs, uint32_t n_segs,

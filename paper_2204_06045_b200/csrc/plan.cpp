@@ -413,10 +413,12 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
             pm_stamp[v] = stamp;
           }
           DevStage& st = hp.stages[unit_stage[u] + stage];
+          st = DevStage{};
           st.nt = static_cast<uint8_t>(o.nin);
           st.main = stage == 0 ? kSegMain : static_cast<uint8_t>(main_pos[g]);
           st.ns = static_cast<uint8_t>(o.ns);
           st.op0 = static_cast<uint8_t>(tix - unit_tref[u]);
+          st.u[0] = st.u[1] = kNoVar;
         }
         double bytes = 16.0 * static_cast<double>(uint64_t{1} << o.r);
         const OpIn* ins = w.inputs(o);
@@ -440,6 +442,25 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
           }
         }
         op_bytes[g] = bytes;
+        if (seg && stage > 0) {  // tabulate P_i when its members are small input tensors
+          DevStage& st = hp.stages[unit_stage[u] + stage];
+          const uint8_t own = static_cast<uint8_t>(kJSrc + (stage - 1));
+          bool ok = st.main == o.nin - 1 && o.nin > 1;
+          int nu = 0;
+          for (int t = 0; ok && t < st.main; ++t) {
+            const OpIn& in = ins[t];
+            const DevTensor& x = hp.trefs[tix - o.nin + t];
+            if (!in.initial || in.rank > 2) { ok = false; break; }
+            for (int ax = 0; ax < x.rank; ++ax) {
+              const uint8_t c = x.src[ax];
+              if (c == own || (nu > 0 && st.u[0] == c) || (nu > 1 && st.u[1] == c)) continue;
+              if (nu == 2) { ok = false; break; }
+              st.u[nu++] = c;
+            }
+          }
+          st.ptab = ok ? 1 : 0;
+          if (!ok) st.u[0] = st.u[1] = kNoVar;
+        }
         // the summed vars of this stage never reappear
         if (seg) for (int k = 0; k < o.ns; ++k) pm_stamp[sv[k]] = 0;
       }
