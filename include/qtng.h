@@ -212,8 +212,9 @@ qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64
                               int64_t* n_out);
 /* Device time of the last qtng_plan_execute summed per kernel kind (ms):
  * ms3[0] level_kernel, ms3[1] outer_kernel, ms3[2] seg_kernel -- CUDA events
- * on the stream each kernel runs on. */
-qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3);
+ * on the stream each kernel runs on.  per_level (optional, cap entries):
+ * the same three times for each level, level-major. */
+qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3, float* per_level, int cap);
 /* Per-level device time of the last qtng_plan_execute (ms), n_levels entries. */
 qtng_status qtng_plan_level_ms(const qtng_plan* plan, float* ms, int cap);
 void qtng_plan_destroy(qtng_plan* plan);

@@ -567,8 +567,15 @@ class Plan:
     def kernel_ms(self) -> dict:
         """Device ms of the last execute() per kernel kind (events on each kernel's stream)."""
         ms = np.zeros(3, np.float32)
-        _check(lib.qtng_plan_kernel_ms(self._h, ms))
+        _check(lib.qtng_plan_kernel_ms(self._h, ms, None, 0))
         return {"level_kernel": float(ms[0]), "outer_kernel": float(ms[1]), "seg_kernel": float(ms[2])}
+
+    def level_kernel_ms(self) -> np.ndarray:
+        """(n_levels, 3) device ms of the last execute(): level / outer / seg kernel per level."""
+        n = self.info().n_levels
+        ms, per = np.zeros(3, np.float32), np.zeros(3 * max(1, n), np.float32)
+        _check(lib.qtng_plan_kernel_ms(self._h, ms, per.ctypes.data_as(C.c_void_p), 3 * n))
+        return per[:3 * n].reshape(n, 3)
 
     def time_level(self, level: int = -1, n_runs: int = 10):
         lv, by, ms = C.c_int(0), C.c_double(0), C.c_float(0)

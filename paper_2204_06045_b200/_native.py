@@ -84,7 +84,7 @@ def _load():
                                     C.POINTER(PlanInfo)]
     lib.qtng_plan_records.argtypes = [vp, C.POINTER(Record), C.c_int64, C.POINTER(C.c_int64)]
     lib.qtng_plan_level_ms.argtypes = [vp, f32p, C.c_int]
-    lib.qtng_plan_kernel_ms.argtypes = [vp, f32p]
+    lib.qtng_plan_kernel_ms.argtypes = [vp, f32p, C.c_void_p, C.c_int]
     lib.qtng_plan_destroy.argtypes = [vp]
     lib.qtng_plan_destroy.restype = None
     lib.qtng_plan_time_level.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_int),

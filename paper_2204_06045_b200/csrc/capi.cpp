@@ -333,6 +333,7 @@ struct qtng_plan {
   std::vector<float> level_ms;
   std::vector<cudaEvent_t> ker_ev;  // 6 per level (enqueue_level)
   float kernel_ms[3] = {0.f, 0.f, 0.f};  // level / outer / segment kernels, last execute
+  std::vector<float> level_kernel_ms;    // 3 per level, last execute
   cudaGraphExec_t graph = nullptr;
   uint64_t graph_gen = ~uint64_t{0};
   ~qtng_plan() {
@@ -723,6 +724,7 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     for (size_t L = 0; L < hp.levels.size(); ++L)
       QTNG_CUDA(cudaEventElapsedTime(&plan->level_ms[L], plan->lev_ev[L], plan->lev_ev[L + 1]));
     for (float& k : plan->kernel_ms) k = 0.f;
+    plan->level_kernel_ms.assign(3 * hp.levels.size(), 0.f);
     for (size_t L = 0; L < hp.levels.size(); ++L) {
       const LevelLaunch& lv = hp.levels[L];
       const uint32_t present[3] = {lv.items, lv.outer_items, lv.seg_items};
@@ -731,6 +733,7 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
         float ms = 0.f;
         QTNG_CUDA(cudaEventElapsedTime(&ms, plan->ker_ev[6 * L + 2 * k], plan->ker_ev[6 * L + 2 * k + 1]));
         plan->kernel_ms[k] += ms;
+        plan->level_kernel_ms[3 * L + k] = ms;
       }
     }
     if (device_ms) *device_ms = ms;
@@ -873,10 +876,13 @@ qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64
   });
 }
 
-qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3) {
+qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3, float* per_level, int cap) {
   return guarded([&] {
     if (!plan || !ms3) throw Error(kInvalidInput, "null argument");
     for (int k = 0; k < 3; ++k) ms3[k] = plan->kernel_ms[k];
+    if (per_level)
+      for (int i = 0; i < cap && i < static_cast<int>(plan->level_kernel_ms.size()); ++i)
+        per_level[i] = plan->level_kernel_ms[i];
   });
 }
 

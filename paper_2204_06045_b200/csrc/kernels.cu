@@ -665,12 +665,14 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
   // ctr[0] = next tile, ctr[1] = finished warps; the last warp resets both
   int cur = -1;
   uint32_t cur_begin = 0, cur_end = 0;
+  bool ptab_fresh = false, ptab_tile = false;
   DevSeg sg{};
+  uint32_t nxt = 0;  // the next tile is fetched while the current one runs
+  if (lane == 0) nxt = atomicAdd(ctr, 1u);
   for (;;) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(ctr, 1u);
-    item = __shfl_sync(kFull, item, 0);
+    const uint32_t item = __shfl_sync(kFull, nxt, 0);
     if (item >= items) break;
+    if (lane == 0) nxt = atomicAdd(ctr, 1u);
     if (cur < 0 || item < cur_begin || item >= cur_end) {
       uint32_t lo = 0, hi = seg_count;
       while (hi - lo > 1) {
@@ -681,6 +683,7 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
         cur = static_cast<int>(lo);
         sg = segs[lo];
         __syncwarp();
+        bool tile_dep = false;
         if (lane < sg.nst) {
           const DevStage st = stages[sg.stage + lane];
           cw.st[lane] = st;
@@ -688,7 +691,12 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
           for (int t = 0; real && t < st.nt - 1; ++t)
             real = __ldg(&segtab[sg.tref + st.op0 + t].kind) == kTensorRealScalar;
           cw.preal[lane] = real ? 1 : 0;
+          for (int w = 0; w < 2; ++w)
+            tile_dep |= st.ptab && st.u[w] >= kTileSrc && st.u[w] < kSumSrc;
         }
+        // the side-product tables depend on the tile only through tile-bit u's
+        ptab_tile = __any_sync(kFull, tile_dep);
+        ptab_fresh = false;
       }
       cur_begin = __ldg(ibeg + lo);
       cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
@@ -700,7 +708,10 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
       const uint32_t sum = __reduce_add_sync(kFull, v);
       if (lane == 0) cw.toff[op] = sum;
     }
-    chain_ptab_build(cw, sg, trefs, arena, tile, lane);
+    if (!ptab_fresh || ptab_tile) {
+      chain_ptab_build(cw, sg, trefs, arena, tile, lane);
+      ptab_fresh = true;
+    }
     __syncwarp();
     const DevStage s1 = cw.st[0];
     switch (s1.nt * 2 + s1.ns) {
