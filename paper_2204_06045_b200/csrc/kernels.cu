@@ -492,9 +492,6 @@ __device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const SegOpTa
 #ifndef QTNG_SEG_PTAB
 #define QTNG_SEG_PTAB 1  // tabulated side products in the climb
 #endif
-#ifndef QTNG_SEG_U2_MAXNT
-#define QTNG_SEG_U2_MAXNT 0  // widest head evaluated in groups of four j (tuned: pairs everywhere)
-#endif
 
 // Index bit of a tabulated side product from var code c (lane / digit bit;
 // tile bits are fixed per tile and folded into the table).
@@ -594,20 +591,109 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
   }
 }
 
+// Tiles of segments whose Y has fewer than 32 outputs (cY < 5; the chain
+// tails): 2^J stage-1 evaluations (NT members, NS summed bits) where the ld = min(5 - cY, J) lowest digits
+// ride on the otherwise idle lanes: lane = (lane digits << cY) | Y bits, and
+// stages 2 .. ld+1 combine sibling lanes with shfl_xor (t0 + t1 == t1 + t0
+// exactly, so every sibling holds the unfused value).  The remaining digits
+// are walked by the loop in pairs (the pair's stage resolved in registers),
+// then the climb parks s_i = 0 terms in shared memory.
+template <int NT, int NS, int K0>
+__device__ __noinline__ void chain_tile_lanes(ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                           const DevSeg& sg, double2* __restrict__ arena,
+                                           uint32_t tile, int lane) {
+  const int L = sg.nst, J = L - 1, cy = sg.cy;
+  const int nld = min(kSegYBits - cy, J);
+  const uint32_t ldig = (static_cast<uint32_t>(lane) >> cy) & ((1u << nld) - 1u);
+  const uint32_t nloop = 1u << (J - nld);
+  const int G = nloop > 1 ? 2 : 1;
+  const double2* B[NT];
+  uint32_t o[NT], sdl[NT], d0[NT], sld[NT];
+  // K0: member 0 is a real scalar r (the |+> state on the summed var): the
+  // first product (r, 0) * M1 becomes a scale, and member 0 is not gathered
+  const double r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : 0.0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const SegOpTab* tb = tab + t;
+    B[t] = arena + __ldg(&tb->off);
+    uint32_t lo = 0, sum = 0;  // lane digits: this lane's part and the sum of their deltas
+    for (int b = 0; b < nld; ++b) {
+      const uint32_t d = __ldg(&tb->dj[b]);
+      lo += ((ldig >> b) & 1u) ? d : 0u;
+      sum += d;
+    }
+    o[t] = cw.toff[t] + __ldg(&tb->llane[lane]) + lo;
+    sld[t] = sum;
+    sdl[t] = __ldg(&tb->sd);
+    d0[t] = G > 1 ? __ldg(&tb->dj[nld]) : 0u;
+  }
+  for (uint32_t j = 0; j < nloop; j += G) {
+    if (j) {  // from j - 2 (low loop bit clear) to j; inc[] assumes every lower digit was set
+      const int b = nld + __ffs(j) - 1;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + sld[t] + d0[t];
+    }
+    double2 v[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (q >= G) break;
+      uint32_t oq[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) oq[t] = o[t] + (q ? d0[t] : 0u);
+      double2 x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
+#pragma unroll
+      for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
+      if (NS) {
+        double2 p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
+#pragma unroll
+        for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
+        x = cadd(x, p);
+      }
+      // lane-digit stages: combine with the sibling lane
+      const uint32_t fj = ((j + q) << nld) | ldig;
+      for (int k = 0; k < nld; ++k) {
+        const double2 t = chain_term(cw, tab, arena, cw.st[k + 1], k, fj, x, lane);
+        const double2 u = make_double2(__shfl_xor_sync(kFull, t.x, 1 << (cy + k)),
+                                       __shfl_xor_sync(kFull, t.y, 1 << (cy + k)));
+        x = cadd(t, u);
+      }
+      v[q] = x;
+    }
+    double2 x = v[0];
+    if (G > 1) {  // the pair's stage (digit nld) in registers
+      const uint32_t f0 = (j << nld) | ldig;
+      x = cadd(chain_term(cw, tab, arena, cw.st[nld + 1], nld, f0, v[0], lane),
+               chain_term(cw, tab, arena, cw.st[nld + 1], nld, f0 | (1u << nld), v[1], lane));
+    }
+    // climb: stage i = k + 2 >= nld + 3 while the carry propagates
+    const uint32_t jj = ((j | (G - 1)) << nld) | ldig;
+    bool carry = true;
+    for (int k = nld + 1; k + 2 <= L; ++k) {
+      const double2 term = chain_term(cw, tab, arena, cw.st[k + 1], k, jj, x, lane);
+      if (!((jj >> k) & 1u)) {
+        cw.acc[k - 1][lane] = term;
+        carry = false;
+        break;
+      }
+      x = cadd(cw.acc[k - 1][lane], term);
+    }
+    if (carry && ldig == 0 && lane < (1 << cy))
+      arena[sg.out + (static_cast<uint64_t>(tile) << cy) + lane] = x;
+  }
+}
+
 template <int NT, int NS>
 __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                              const DevSeg& sg, double2* __restrict__ arena,
                                              uint32_t tile, int lane) {
-  // wide heads use pairs of j (register pressure), the rest groups of four
   const bool k0 = NT >= 2 && __ldg(&tab[0].kind) == kTensorRealScalar;
-  constexpr int U = NT <= QTNG_SEG_U2_MAXNT ? 2 : 1;
-  if (U == 2 && sg.nst >= 3) {
-    if (k0) chain_tile<NT, NS, U, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
-    else chain_tile<NT, NS, U, 0>(cw, tab, sg, arena, tile, lane);
-  } else {
-    if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
-    else chain_tile<NT, NS, 1, 0>(cw, tab, sg, arena, tile, lane);
+  if (sg.cy < kSegYBits) {  // chain tails: digits on the idle lanes
+    if (k0) chain_tile_lanes<NT, NS, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+    else chain_tile_lanes<NT, NS, 0>(cw, tab, sg, arena, tile, lane);
+    return;
   }
+  if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+  else chain_tile<NT, NS, 1, 0>(cw, tab, sg, arena, tile, lane);
 }
 
 // Tabulate the side products of the fused stages for this tile: lane
