@@ -118,10 +118,16 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   // main_pos[g]: position of op g's fused main member, -1 when g heads its unit
   std::vector<int8_t> main_pos(N, -1);
   std::vector<uint32_t> unit_of(N);
-  std::vector<uint32_t> unit_first, unit_last, unit_len, unit_nops;  // per unit
   std::vector<uint32_t> next_in_unit(N, ~0u);
-  for (int c = 0; c < C; ++c) {
+  // per cone in parallel (units never span lightcones), cone-local unit ids
+  struct ConeUnits {
+    std::vector<uint32_t> first, last, len, nops;
+    int max_level = -1;
+  };
+  std::vector<ConeUnits> cus(C);
+  Pool::get().parallel_for(C, [&](int c) {
     const WalkResult& w = *cones[c];
+    ConeUnits& cu = cus[c];
     for (uint32_t k = 0; k < w.ops.size(); ++k) {
       const uint32_t g = base[c] + k;
       const Op& o = w.ops[k];
@@ -134,42 +140,51 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       }
       if (t_main >= 0) {
         const uint32_t pg = base[c] + static_cast<uint32_t>(w.inputs(o)[t_main].ref);
-        const Op& p = op_at(pg);
+        const Op& p = w.ops[pg - base[c]];
         const uint32_t u = unit_of[pg];
-        const bool head_ok = unit_len[u] > 1 || (p.ns <= 1 && p.nin <= kSegMaxNt1);
-        const int L = static_cast<int>(unit_len[u]) + 1;
-        if (head_ok && unit_last[u] == pg && L - 1 <= seg_max_j() &&
-            unit_nops[u] + static_cast<uint32_t>(o.nin) <= static_cast<uint32_t>(kSegMaxOps)) {
+        const bool head_ok = cu.len[u] > 1 || (p.ns <= 1 && p.nin <= kSegMaxNt1);
+        const int L = static_cast<int>(cu.len[u]) + 1;
+        if (head_ok && cu.last[u] == pg && L - 1 <= seg_max_j() &&
+            cu.nops[u] + static_cast<uint32_t>(o.nin) <= static_cast<uint32_t>(kSegMaxOps)) {
           main_pos[g] = static_cast<int8_t>(t_main);
           unit_of[g] = u;
           next_in_unit[pg] = g;
-          unit_last[u] = g;
-          ++unit_len[u];
-          unit_nops[u] += static_cast<uint32_t>(o.nin);
+          cu.last[u] = g;
+          ++cu.len[u];
+          cu.nops[u] += static_cast<uint32_t>(o.nin);
           continue;
         }
       }
-      unit_of[g] = static_cast<uint32_t>(unit_first.size());
-      unit_first.push_back(g);
-      unit_last.push_back(g);
-      unit_len.push_back(1);
-      unit_nops.push_back(static_cast<uint32_t>(o.nin));
+      unit_of[g] = static_cast<uint32_t>(cu.first.size());
+      cu.first.push_back(g);
+      cu.last.push_back(g);
+      cu.len.push_back(1);
+      cu.nops.push_back(static_cast<uint32_t>(o.nin));
     }
-  }
-  const uint32_t U = static_cast<uint32_t>(unit_first.size());
+  });
+  std::vector<uint32_t> ubase(C + 1, 0);
+  for (int c = 0; c < C; ++c) ubase[c + 1] = ubase[c] + static_cast<uint32_t>(cus[c].first.size());
+  const uint32_t U = ubase[C];
+  std::vector<uint32_t> unit_first(U), unit_last(U), unit_len(U), unit_nops(U);
   // unit levels: 1 + the deepest unit producing a materialised input; units
   // are visited in the order of their last op (producers come first)
   std::vector<int32_t> unit_level(U, 0);
-  int max_level = -1;
-  for (int c = 0; c < C; ++c) {
+  Pool::get().parallel_for(C, [&](int c) {
+    ConeUnits& cu = cus[c];
+    const uint32_t ub = ubase[c];
+    std::copy(cu.first.begin(), cu.first.end(), unit_first.begin() + ub);
+    std::copy(cu.last.begin(), cu.last.end(), unit_last.begin() + ub);
+    std::copy(cu.len.begin(), cu.len.end(), unit_len.begin() + ub);
+    std::copy(cu.nops.begin(), cu.nops.end(), unit_nops.begin() + ub);
     const WalkResult& w = *cones[c];
+    for (uint32_t k = 0; k < w.ops.size(); ++k) unit_of[base[c] + k] += ub;
     for (uint32_t k = 0; k < w.ops.size(); ++k) {
       const uint32_t g = base[c] + k;
       const uint32_t u = unit_of[g];
       if (unit_last[u] != g) continue;
       int lvl = 0;
       for (uint32_t s = unit_first[u]; s != ~0u; s = next_in_unit[s]) {
-        const Op& o = op_at(s);
+        const Op& o = w.ops[s - base[c]];
         const OpIn* ins = w.inputs(o);
         for (int t = 0; t < o.nin; ++t) {
           if (ins[t].initial || t == main_pos[s]) continue;
@@ -177,9 +192,11 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
         }
       }
       unit_level[u] = lvl;
-      max_level = std::max(max_level, lvl);
+      cu.max_level = std::max(cu.max_level, lvl);
     }
-  }
+  });
+  int max_level = -1;
+  for (const ConeUnits& cu : cus) max_level = std::max(max_level, cu.max_level);
   const int n_levels = max_level + 1;
   auto level_of = [&](uint32_t g) { return unit_level[unit_of[g]]; };
   auto consumer_unit = [&](uint32_t u) -> int64_t {
