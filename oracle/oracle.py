@@ -150,8 +150,19 @@ def ref_lib():
                                             C.c_int, _i32p, _i32p, _f64p, C.c_long]
         lib.ref_contract_bucket_capped.argtypes = [C.c_int, _i32p, _i32p, C.c_int, _i32p,
                                                    C.c_int]
+        lib.ref_read_timing_csv.argtypes = [C.c_char_p, C.POINTER(C.c_long), C.POINTER(C.c_long),
+                                            C.POINTER(C.c_double)]
         _rlib = lib
     return _rlib
+
+
+def ref_read_timing_csv(text: str):
+    """The reference's read_timing_csv on `text`: (n_records, sum width, sum ops)."""
+    n, w, o = C.c_long(0), C.c_long(0), C.c_double(0)
+    code = ref_lib().ref_read_timing_csv(text.encode(), C.byref(n), C.byref(w), C.byref(o))
+    if code:
+        _ref_err(code)
+    return n.value, w.value, o.value
 
 
 def _ref_err(code):

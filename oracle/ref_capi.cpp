@@ -13,6 +13,7 @@
 //   NaiveBackend/Matmul/Mixed::contract   proj/src/engine.cpp:68-156
 //   simulate_widths         proj/src/engine.cpp:235-240
 //   run_ansatz/expectation_cost           proj/src/statevector.cpp:55-84
+//   read_timing_csv         proj/src/engine.cpp:575-601
 //
 // Nothing here re-implements reference behaviour; it only marshals arrays.
 
@@ -23,6 +24,7 @@
 #include <cstring>
 #include <exception>
 #include <random>
+#include <sstream>
 #include <memory>
 #include <string>
 #include <thread>
@@ -337,6 +339,25 @@ int ref_acceptance_instances(int* ns, uint64_t* seeds, int* ps, double* angles /
     ++i;
   }
   return i;
+}
+
+// read_timing_csv (proj/src/engine.cpp:575-601) on a CSV text: the number of
+// records and the sums of their widths and ops, or the reference's error.
+int ref_read_timing_csv(const char* text, long* n_records, long* width_sum, double* ops_sum) {
+  try {
+    std::istringstream in(text);
+    const std::vector<TimingRecord> recs = read_timing_csv(in);
+    *n_records = static_cast<long>(recs.size());
+    *width_sum = 0;
+    *ops_sum = 0;
+    for (const TimingRecord& r : recs) {
+      *width_sum += r.width;
+      *ops_sum += static_cast<double>(r.ops);
+    }
+    return 0;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
 }
 
 }  // extern "C"

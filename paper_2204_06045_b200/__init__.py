@@ -24,7 +24,7 @@ from ._native import PlanInfo, Record, lib
 __all__ = [
     "InvalidInputError", "GenerationError", "ResourceError", "ScheduleError", "NumericalError",
     "CudaError", "Graph", "Edge", "Angles", "Tensor", "Bucket", "ContractionSchedule",
-    "TimingRecord", "ContractionReport", "EnergyResult", "EngineConfig", "Context",
+    "TimingRecord", "write_timing_csv", "read_timing_csv", "ContractionReport", "EnergyResult", "EngineConfig", "Context",
     "GpuBackend", "Plan", "make_graph", "random_regular", "edge_schedule", "simulate_widths",
     "edge_costs", "validate_energy", "contract_bucket", "contract_network", "energy_expectation",
     "default_context", "version",
@@ -220,6 +220,41 @@ class TimingRecord:
     elapsed_s: float
     ops: int
     flops_est: float
+
+
+_CSV_HEADER = "edge_u,edge_v,bucket_seq,width,backend,elapsed_s,ops,flops_est"
+
+
+def _fmt_g6(x: float) -> str:
+    """std::ostream's default double formatting (%g, precision 6)."""
+    return "%g" % x
+
+
+def write_timing_csv(records: Sequence["TimingRecord"], f) -> None:
+    """write_timing_csv (proj/src/engine.cpp:567-573): same header, field order
+    and default stream formatting, so the reference's report tooling reads it."""
+    f.write(_CSV_HEADER + "\n")
+    for r in records:
+        f.write(f"{r.edge_u},{r.edge_v},{r.bucket_seq},{r.width},{r.backend},"
+                f"{_fmt_g6(r.elapsed_s)},{r.ops},{_fmt_g6(r.flops_est)}\n")
+
+
+def read_timing_csv(f) -> List["TimingRecord"]:
+    """read_timing_csv (proj/src/engine.cpp:575-601), same errors."""
+    lines = f.read().split("\n")
+    if not lines or lines == [""]:
+        raise InvalidInputError("timing CSV: missing header")
+    out = []
+    for line in lines[1:]:
+        if not line:
+            continue
+        fields = line.split(",")
+        if len(fields) < 8:
+            raise InvalidInputError("timing CSV: short row: " + line)
+        u, v, seq, w, backend, el, ops, fl = fields[:8]
+        out.append(TimingRecord(int(u), int(v), int(seq), int(w), backend, float(el), int(ops),
+                                float(fl)))
+    return out
 
 
 @dataclass
