@@ -196,6 +196,16 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
  * throughput measurement; n_runs back-to-back runs, total device time. */
 qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms);
 qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info);
+/* State-vector oracle on the device: run_ansatz + expectation_cost
+ * (proj/src/statevector.cpp:55-90) for n <= cap qubits (the reference's
+ * default cap is 24; the device holds up to 33: 2^33 complex128 = 128 GiB).
+ * The amplitudes are bit-identical to run_ansatz's; the sums over basis
+ * states are reassociated.  zz (optional, m entries): <Z_u Z_v> per edge in
+ * edge order.  Refusals: ResourceError "state vector of N qubits exceeds cap C". */
+qtng_status qtng_statevector_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
+                                    const double* gammas, const double* betas, int cap,
+                                    double* energy, double* zz);
+
 /* Host-only analysis of the fused-chain segments of the plan for all m
  * edges.  Per segment (level-sorted): level, L (stages), rY, cY, nops; then
  * per stage: nt, ns, main (-1 for stage 1), and per member: rank,

@@ -27,7 +27,7 @@ __all__ = [
     "TimingRecord", "write_timing_csv", "read_timing_csv", "ContractionReport", "EnergyResult", "EngineConfig", "Context",
     "GpuBackend", "Plan", "make_graph", "random_regular", "edge_schedule", "simulate_widths",
     "edge_costs", "validate_energy", "contract_bucket", "contract_network", "energy_expectation",
-    "default_context", "version",
+    "default_context", "version", "statevector_energy",
 ]
 
 
@@ -477,6 +477,22 @@ def plan_segments(g: Graph, p: int, merged: bool = False,
             stages.append((nt, ns, main, mem))
         out.append(dict(level=lv, L=L, ry=ry, cy=cy, nops=nops, stages=stages))
     return out
+
+
+def statevector_energy(g: Graph, angles: Angles, cap: int = 24,
+                       ctx: Optional[Context] = None):
+    """The state-vector oracle on the device (run_ansatz + expectation_cost,
+    proj/src/statevector.cpp:55-90): (energy, per-edge <Z_u Z_v>).  cap: the
+    reference's qubit cap (default 24, StateVector::kDefaultCap); the device
+    holds up to 33 qubits."""
+    ctx = ctx or default_context()
+    angles.validate()
+    gam, bet = angles.arrays()
+    e = C.c_double(0.0)
+    zz = np.zeros(max(1, g.m), np.float64)
+    _check(lib.qtng_statevector_energy(ctx.handle, g.n, g.m, g.flat(), angles.depth(), gam, bet,
+                                       int(cap), C.byref(e), zz.ctypes.data_as(C.c_void_p)))
+    return e.value, zz[: g.m]
 
 
 def validate_energy(g: Graph, p: int, merged: bool = False,

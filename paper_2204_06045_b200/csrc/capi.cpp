@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -18,6 +19,7 @@
 #include "kernels.cuh"
 #include "plan.hpp"
 #include "pool.hpp"
+#include "sv.cuh"
 
 using namespace qtng;
 
@@ -204,6 +206,7 @@ struct qtng_ctx {
   cudaStream_t stream3 = nullptr;  // fused-chain segment kernels, forked per level
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, join3_ev = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DevBuf sv_scratch;     // state-vector oracle: edge bits, per-edge sums, partials
 
   void ensure_arena(uint64_t elems) {
     const size_t bytes = std::max<uint64_t>(elems, 32) * sizeof(double2);
@@ -850,6 +853,55 @@ qtng_status qtng_plan_stats(int n, int m, const int* edges, int p, int merged,
     const HostPlan hp =
         build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse != 0, true);
     fill_info(hp, static_cast<int>(ptrs.size()), info);
+  });
+}
+
+qtng_status qtng_statevector_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
+                                    const double* gammas, const double* betas, int cap,
+                                    double* energy, double* zz_out) {
+  return guarded([&] {
+    if (!ctx || !energy) throw Error(kInvalidInput, "null argument");
+    if (p < 1) throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+    const Graph g = graph_from(n, m, edges);
+    // StateVector::plus_state (proj/src/statevector.cpp:9-17)
+    if (n < 1) throw Error(kInvalidInput, "state vector needs at least one qubit");
+    if (n > cap)
+      throw Error(kResource, "state vector of " + std::to_string(n) + " qubits exceeds cap " +
+                                 std::to_string(cap));
+    if (n > 33) throw Error(kResource, "state vector of " + std::to_string(n) +
+                                           " qubits exceeds the device limit 33");
+    const int me = static_cast<int>(g.edges.size());
+    std::vector<int2> bits(me);
+    for (int e = 0; e < me; ++e) bits[e] = int2{n - 1 - g.edges[e].u, n - 1 - g.edges[e].v};
+    std::vector<double2> w(p), c(p), ms(p);
+    for (int k = 0; k < p; ++k) {  // the reference's gate values (statevector.cpp:29,37-38)
+      const std::complex<double> wk = std::exp(std::complex<double>{0.0, -gammas[k]});
+      w[k] = double2{wk.real(), wk.imag()};
+      c[k] = double2{std::cos(betas[k]), 0.0};
+      ms[k] = double2{0.0, -std::sin(betas[k])};
+    }
+    const double amp0 = 1.0 / std::sqrt(static_cast<double>(uint64_t{1} << n));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    ctx->ensure_arena(uint64_t{1} << n);
+    ctx->sv_scratch.ensure(sv_scratch_bytes(std::max(me, 1)));
+    char* scr = static_cast<char*>(ctx->sv_scratch.p);
+    if (me)
+      QTNG_CUDA(cudaMemcpyAsync(scr, bits.data(), sizeof(int2) * me, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    double* zz_dev = reinterpret_cast<double*>(scr + sizeof(int2) * me);
+    QTNG_CUDA(sv_run(ctx->stream, ctx->A(), n, me, reinterpret_cast<const int2*>(scr), p, w.data(),
+                     c.data(), ms.data(), amp0, scr, zz_dev));
+    std::vector<double> zz(me);
+    if (me)
+      QTNG_CUDA(cudaMemcpyAsync(zz.data(), zz_dev, sizeof(double) * me, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    // expectation_cost (statevector.cpp:86-90): m/2 - 1/2 sum, edge order
+    double sum = 0.0;
+    for (double x : zz) sum += x;
+    *energy = 0.5 * static_cast<double>(me) - 0.5 * sum;
+    if (zz_out) std::copy(zz.begin(), zz.end(), zz_out);
   });
 }
 
