@@ -209,7 +209,8 @@ qtng_status qtng_statevector_energy(qtng_ctx* ctx, int n, int m, const int* edge
 /* Host-only analysis of the fused-chain segments of the plan for all m
  * edges.  Per segment (level-sorted): level, L (stages), rY, cY, nops; then
  * per stage: nt, ns, main (-1 for stage 1), and per member: rank,
- * initial (1 = gate / input-region tensor; a main placeholder has rank 0).
+ * initial (1 = gate / input-region tensor; a main placeholder has rank 0),
+ * then its rank axis codes (device_plan.hpp: lane / digit / tile / summed bit).
  * *n_ints receives the size needed; nothing is written if cap is short. */
 qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged,
                                int max_result_width, int* ints, int64_t cap, int64_t* n_ints);

@@ -455,7 +455,7 @@ def plan_stats(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfi
 def plan_segments(g: Graph, p: int, merged: bool = False,
                   cfg: Optional[EngineConfig] = None) -> List[dict]:
     """Host-only description of the fused-chain segments of Plan(g, p):
-    level, L, ry, cy, nops, stages=[(nt, ns, main, [(rank, initial)])]."""
+    level, L, ry, cy, nops, stages=[(nt, ns, main, [(rank, initial, codes)])]."""
     cfg = cfg or EngineConfig()
     n_ints = C.c_int64(0)
     probe = np.zeros(1, np.int32)
@@ -472,8 +472,11 @@ def plan_segments(g: Graph, p: int, merged: bool = False,
         for _ in range(L):
             nt, ns, main = (int(x) for x in buf[i:i + 3])
             i += 3
-            mem = [(int(buf[i + 2 * t]), int(buf[i + 2 * t + 1])) for t in range(nt)]
-            i += 2 * nt
+            mem = []
+            for _ in range(nt):
+                rank, ini = int(buf[i]), int(buf[i + 1])
+                mem.append((rank, ini, [int(x) for x in buf[i + 2:i + 2 + rank]]))
+                i += 2 + rank
             stages.append((nt, ns, main, mem))
         out.append(dict(level=lv, L=L, ry=ry, cy=cy, nops=nops, stages=stages))
     return out

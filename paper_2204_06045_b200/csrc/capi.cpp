@@ -828,6 +828,7 @@ qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged
             const DevTensor& x = hp.trefs[sg.tref + st.op0 + t];
             out.push_back(x.rank);
             out.push_back(x.rank && x.off < hp.input_elems ? 1 : 0);
+            for (int ax = 0; ax < x.rank; ++ax) out.push_back(x.src[ax]);
           }
         }
       }

@@ -68,7 +68,7 @@ def test_segment_shapes(q, golden):
         for nt, ns, main, mem in s["stages"][1:]:
             assert ns == 1 and nt <= 4 and main == nt - 1
             assert mem[main][0] == 0  # placeholder: read from registers
-            assert all(rank > 0 for rank, _ in mem[:main])
+            assert all(rank > 0 for rank, _, _ in mem[:main])
         # stage i's result rank shrinks by its summed var: rY = r_1 - (L - 1)
 
 
