@@ -69,13 +69,13 @@ def committed_traffic(kernel):
     return {"traffic": None}
 
 
-def fp64_pipe_peak(dev_index, sm_max_mhz):
+def fp64_pipe_peak(dev_index, sm_max_mhz, lanes=64):
     """FP64 pipe issue peak in op/s: SMs x 64 FP64 lanes x SM clock.  The
     bucket loop is DMUL/DADD (one op per lane per clock each); NVIDIA's 37
-    TFLOP/s figure counts a DFMA as two."""
+    TFLOP/s figure counts a DFMA as two.  lanes=128: the FP32 pipe (c64 mode)."""
     import torch
     sms = torch.cuda.get_device_properties(dev_index).multi_processor_count
-    return sms * 64 * (sm_max_mhz or 1965.0) * 1e6, sms
+    return sms * lanes * (sm_max_mhz or 1965.0) * 1e6, sms
 
 
 def golden_energy(name):
@@ -237,7 +237,8 @@ def run_b200(args, cfg):
     costs = q.edge_costs(g, p)
     shards = qd.lpt_shard(costs, world)
     mine = shards[rank]
-    plan = q.Plan(g, p, edges=mine, ctx=ctx)
+    ecfg = q.EngineConfig(dtype=args.dtype)
+    plan = q.Plan(g, p, edges=mine, ctx=ctx, cfg=ecfg)
     info = plan.info()
 
     def energy_step_device():
@@ -268,11 +269,11 @@ def run_b200(args, cfg):
         barrier()
         # ---- e2e: public API with host inputs
         for _ in range(max(1, args.warmup // 2)):
-            q.energy_expectation(g, a, q.GpuBackend(ctx), edges=mine)
+            q.energy_expectation(g, a, q.GpuBackend(ctx), edges=mine, cfg=ecfg)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            res = q.energy_expectation(g, a, q.GpuBackend(ctx), edges=mine)
+            res = q.energy_expectation(g, a, q.GpuBackend(ctx), edges=mine, cfg=ecfg)
             if world > 1:
                 qd.reduce_terms(qd.scatter_terms(g.m, mine, res.terms), dev)
         barrier()
@@ -303,7 +304,8 @@ def run_b200(args, cfg):
     value = g.m * args.steps / (total_ms / 1e3)
     gold = golden_energy(args.config)
     csum = clocks.summary()
-    fp_peak, sms = fp64_pipe_peak(local, csum.get("sm_max_mhz"))
+    c64 = args.dtype == "c64"
+    fp_peak, sms = fp64_pipe_peak(local, csum.get("sm_max_mhz"), 128 if c64 else 64)
     seg_s = kms["seg_kernel"] / 1e3
     lvl_s = kms["level_kernel"] / 1e3
     seg_ach = info.seg_fp64_ops / seg_s / 1e12 if seg_s > 0 else None
@@ -311,14 +313,15 @@ def run_b200(args, cfg):
     out = {
         "metric": METRIC, "value": value, "unit": "lightcones/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (seeded random 3-regular graph, acceptance-scale angles)",
         "config": {"workload": cfg["workload"], "parallelism": f"lightcone-sharded x{world}",
                    "l2": "512 MiB flush between timed steps (outside the timed region)",
                    "buckets": int(info.n_buckets), "levels": int(info.n_levels),
                    "max_width": int(info.max_width)},
         "energy": energy, "energy_golden_naive": gold,
-        "parity_bit_exact": (energy == gold) if gold is not None else None,
+        "parity_bit_exact": (energy == gold) if gold is not None and args.dtype == "c128" else None,
+        "parity_rel_err": (abs(energy - gold) / abs(gold)) if gold else None,
         "e2e": {"value": g.m * args.steps / e2e_s, "unit": "lightcones/s",
                 "h2d_bytes_per_step": int(info.desc_bytes + 16 * (2 + 4 * p) * 4),
                 "d2h_bytes_per_step": int(16 * len(mine)),
@@ -332,11 +335,12 @@ def run_b200(args, cfg):
                                         "(schedules/descriptors built once per graph)"},
         # dominant kernel: the fused-chain seg_kernel keeps every chain
         # intermediate in registers, so it is bound by the FP64 pipe, not HBM
-        "roofline": {"bound": "fp64", "kernel": "seg_kernel (all levels)",
+        "roofline": {"bound": "fp32" if c64 else "fp64", "kernel": "seg_kernel (all levels)",
                      "achieved": seg_ach, "peak": fp_peak / 1e12, "unit": "TFLOP/s",
                      "frac": (seg_ach * 1e12 / fp_peak) if seg_ach else None,
-                     "peak_source": f"derived: {sms} SMs x 64 FP64 lanes x sm_max_mhz "
-                                    "(DMUL/DADD issue rate; NVIDIA's FP64 figure counts DFMA as 2)",
+                     "peak_source": (f"derived: {sms} SMs x 128 FP32 lanes x sm_max_mhz" if c64 else
+                                     f"derived: {sms} SMs x 64 FP64 lanes x sm_max_mhz "
+                                     "(DMUL/DADD issue rate; NVIDIA's FP64 figure counts DFMA as 2)"),
                      **committed_traffic("seg_kernel"),
                      "flops_per_step": info.seg_fp64_ops,
                      "flops_def": "the reference NaiveBackend loop's FP64 mul+add count of the "
@@ -407,6 +411,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtype", choices=["c128", "c64"], default="c128",
+                    help="c64: the optional complex64 mode (1e-5), not the headline")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = dict(CONFIGS[args.config])

@@ -91,6 +91,12 @@ typedef struct qtng_plan_info {
  * (0 = grow on demand). */
 qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out);
 void qtng_destroy(qtng_ctx* ctx);
+/* Arithmetic of the QAOA plans and energies created on ctx from now on:
+ * 128 (default) = complex128, bit-identical to the reference's naive backend;
+ * 64 = complex64 arena and kernels (the north_star's optional mode, results
+ * within 1e-5; complex128 per-lightcone products).  Explicit schedules and
+ * single buckets always run in complex128. */
+qtng_status qtng_set_precision(qtng_ctx* ctx, int bits);
 /* Message of the calling thread's last failure ("" after success). */
 const char* qtng_last_error(void);
 /* Library build string (arch, version). */

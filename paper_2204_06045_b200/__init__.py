@@ -11,6 +11,7 @@ CUDA for sm_100a).  There is no CPU fallback.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
@@ -155,6 +156,14 @@ class EngineConfig:
     """EngineConfig (engine.hpp:16-20)."""
 
     max_result_width: int = 30
+    # "c128" (default): bit-identical to the reference's naive backend;
+    # "c64": complex64 arena and arithmetic (north_star tolerance 1e-5)
+    dtype: str = "c128"
+
+    def precision_bits(self) -> int:
+        if self.dtype not in ("c128", "c64"):
+            raise InvalidInputError("dtype must be 'c128' or 'c64'")
+        return 128 if self.dtype == "c128" else 64
 
     @staticmethod
     def from_env() -> "EngineConfig":
@@ -279,6 +288,17 @@ class Context:
         _check(lib.qtng_create(device, arena_bytes, C.byref(h)))
         self._h = h
         self.device = device
+        self._prec_lock = threading.Lock()
+
+    @contextlib.contextmanager
+    def precision(self, bits: int):
+        """Plans and energies created inside use complex`bits` (128 or 64)."""
+        with self._prec_lock:
+            _check(lib.qtng_set_precision(self.handle, int(bits)))
+            try:
+                yield self
+            finally:
+                _check(lib.qtng_set_precision(self.handle, 128))
 
     @property
     def handle(self):
@@ -538,10 +558,11 @@ def energy_expectation(g: Graph, angles: Angles, backend: Optional[GpuBackend] =
     k = g.m if sel is None else len(sel)
     terms = np.zeros(2 * max(1, k), np.float64)
     e = C.c_double(0)
-    _check(lib.qtng_energy(ctx.handle, g.n, g.m, g.flat(), angles.depth(), gam, bet, int(merged),
-                           cfg.max_result_width, k,
-                           None if sel is None else sel.ctypes.data_as(C.c_void_p),
-                           C.byref(e), terms))
+    with ctx.precision(cfg.precision_bits()):
+        _check(lib.qtng_energy(ctx.handle, g.n, g.m, g.flat(), angles.depth(), gam, bet,
+                               int(merged), cfg.max_result_width, k,
+                               None if sel is None else sel.ctypes.data_as(C.c_void_p),
+                               C.byref(e), terms))
     return EnergyResult(e.value, terms[: 2 * k].view(np.complex128).copy())
 
 
@@ -562,9 +583,10 @@ class Plan:
         self.sel = (np.arange(g.m, dtype=np.int32) if edges is None
                     else np.ascontiguousarray(edges, dtype=np.int32))
         h = C.c_void_p()
-        _check(lib.qtng_plan_create(self.ctx.handle, g.n, g.m, g.flat(), p, int(merged),
-                                    cfg.max_result_width, len(self.sel),
-                                    self.sel.ctypes.data_as(C.c_void_p), C.byref(h)))
+        with self.ctx.precision(cfg.precision_bits()):
+            _check(lib.qtng_plan_create(self.ctx.handle, g.n, g.m, g.flat(), p, int(merged),
+                                        cfg.max_result_width, len(self.sel),
+                                        self.sel.ctypes.data_as(C.c_void_p), C.byref(h)))
         self._h = h
         self.last_device_ms = 0.0
 

@@ -207,9 +207,11 @@ struct qtng_ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, join3_ev = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf sv_scratch;     // state-vector oracle: edge bits, per-edge sums, partials
+  int prec = 128;        // QAOA plans / energies: 128 = complex128, 64 = complex64
 
-  void ensure_arena(uint64_t elems) {
-    const size_t bytes = std::max<uint64_t>(elems, 32) * sizeof(double2);
+  // arena of `elems` elements of `elem_bytes` (16: double2, 8: float2)
+  void ensure_arena(uint64_t elems, size_t elem_bytes = sizeof(double2)) {
+    const size_t bytes = std::max<uint64_t>(elems, 32) * elem_bytes;
     if (bytes > arena.cap) {
       size_t free_b = 0, total_b = 0;
       cudaMemGetInfo(&free_b, &total_b);
@@ -228,6 +230,7 @@ namespace {
 struct DevProgram {
   char* base = nullptr;
   DescLayout L;
+  bool c64 = false;  // complex64 arena (float2) and kernels
   const DevOp* ops() const { return reinterpret_cast<const DevOp*>(base + L.ops); }
   const uint32_t* ibeg() const { return reinterpret_cast<const uint32_t*>(base + L.ibeg); }
   const DevTensor* trefs() const { return reinterpret_cast<const DevTensor*>(base + L.trefs); }
@@ -246,7 +249,8 @@ struct DevProgram {
 // kev (optional): 6 events bracketing this level's level / outer / segment
 // kernels on the streams they run on (per-kernel device time).
 void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const DevProgram& pr,
-                   double2* arena, cudaEvent_t* kev = nullptr) {
+                   void* arena, cudaEvent_t* kev = nullptr) {
+  const bool c64 = pr.c64;
   const bool fork2 = lv.outer_items > 0;
   const bool fork3 = lv.seg_items > 0 && (lv.items > 0 || fork2);
   auto rec = [&](int k, cudaStream_t st) {
@@ -256,22 +260,39 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
   if (fork2) {
     QTNG_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->fork_ev, 0));
     rec(2, ctx->stream2);
-    QTNG_CUDA(launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+    QTNG_CUDA(c64 ? c64::launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv)
+                  : c128::launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
     rec(3, ctx->stream2);
     QTNG_CUDA(cudaEventRecord(ctx->join_ev, ctx->stream2));
   }
   cudaStream_t s3 = fork3 ? ctx->stream3 : ctx->stream;
   if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream3, ctx->fork_ev, 0));
   rec(4, s3);
-  QTNG_CUDA(launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(), pr.segtab(), arena,
-                        pr.ctr(level), lv));
+  QTNG_CUDA(c64 ? c64::launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
+                                    pr.segtab(), arena, pr.ctr(level), lv)
+                : c128::launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
+                                    pr.segtab(), arena, pr.ctr(level), lv));
   rec(5, s3);
   if (fork3) QTNG_CUDA(cudaEventRecord(ctx->join3_ev, ctx->stream3));
   rec(0, ctx->stream);
-  QTNG_CUDA(launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+  QTNG_CUDA(c64 ? c64::launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv)
+                : c128::launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
   rec(1, ctx->stream);
   if (fork2) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join3_ev, 0));
+}
+
+size_t elem_bytes(const HostPlan& hp) { return hp.c64 ? sizeof(float2) : sizeof(double2); }
+
+// Copy `elems` complex128 inputs (interleaved re, im) into a pinned staging
+// buffer in the plan's element type.
+void stage_input(const HostPlan& hp, const double* in, uint64_t elems, void* dst) {
+  if (!hp.c64) {
+    std::memcpy(dst, in, elems * sizeof(double2));
+    return;
+  }
+  float* f = static_cast<float*>(dst);
+  for (uint64_t i = 0; i < 2 * elems; ++i) f[i] = static_cast<float>(in[i]);
 }
 
 // Upload a HostPlan's descriptor image to `dev` (layout L) on the context
@@ -280,14 +301,14 @@ void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* d
   ctx->pin_desc.ensure(L.upload);
   pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
   QTNG_CUDA(cudaMemcpyAsync(dev, ctx->pin_desc.p, L.upload, cudaMemcpyHostToDevice, ctx->stream));
-  const DevProgram pr{dev, L};
-  QTNG_CUDA(launch_seg_prep(ctx->stream, pr.segs(), static_cast<uint32_t>(hp.segs.size()), pr.trefs(),
+  const DevProgram pr{dev, L, hp.c64};
+  QTNG_CUDA(c128::launch_seg_prep(ctx->stream, pr.segs(), static_cast<uint32_t>(hp.segs.size()), pr.trefs(),
                             pr.segtab()));
 }
 
 // Enqueue the whole program on the context's stream: every level, then the
 // per-lightcone products.
-void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, double2* arena,
+void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, void* arena,
                      std::vector<cudaEvent_t>* level_events,
                      std::vector<cudaEvent_t>* kernel_events = nullptr) {
   cudaStream_t s = ctx->stream;
@@ -297,7 +318,8 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, do
                   kernel_events ? kernel_events->data() + 6 * L : nullptr);
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
-  QTNG_CUDA(launch_final(s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
+  QTNG_CUDA((pr.c64 ? c64::launch_final : c128::launch_final)(
+      s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
                          arena, pr.terms()));
 }
 
@@ -312,9 +334,13 @@ int launches_per_run(const HostPlan& hp) {
 }
 
 // Ops of the reference's run_edge post-processing (engine.cpp:517-519, 543-546).
-void check_terms(const std::vector<Edge>& edges, const double* terms) {
+// |imag e_jk| bound: the reference's 1e-8 (engine.cpp:517-519); complex64
+// plans use the north_star's 1e-5.
+double imag_tol(bool c64) { return c64 ? 1e-5 : 1e-8; }
+
+void check_terms(const std::vector<Edge>& edges, const double* terms, double tol = 1e-8) {
   for (size_t i = 0; i < edges.size(); ++i)
-    if (std::abs(terms[2 * i + 1]) > 1e-8)
+    if (std::abs(terms[2 * i + 1]) > tol)
       throw Error(kSchedule, "edge (" + std::to_string(edges[i].u) + ", " +
                                  std::to_string(edges[i].v) +
                                  "): edge term has non-real value: imag = " +
@@ -386,6 +412,15 @@ void qtng_destroy(qtng_ctx* ctx) {
   if (s) cudaStreamDestroy(s);
   if (s2) cudaStreamDestroy(s2);
   if (s3) cudaStreamDestroy(s3);
+}
+
+qtng_status qtng_set_precision(qtng_ctx* ctx, int bits) {
+  return guarded([&] {
+    if (!ctx) throw Error(kInvalidInput, "null context");
+    if (bits != 128 && bits != 64) throw Error(kInvalidInput, "precision must be 128 or 64 bits");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->prec = bits;
+  });
 }
 
 qtng_status qtng_random_regular(int n, int d, uint64_t seed, int* edges, int cap, int* m_out) {
@@ -514,15 +549,16 @@ namespace {
 void run_program_once(qtng_ctx* ctx, const HostPlan& hp, const double* input,
                       uint64_t input_elems, double2* terms_host) {
   const DescLayout L = layout_of(hp);
-  ctx->ensure_arena(std::max(hp.arena_elems, input_elems));
+  const size_t eb = elem_bytes(hp);
+  ctx->ensure_arena(std::max(hp.arena_elems, input_elems), eb);
   ctx->desc.ensure(L.total);
-  ctx->pin_in.ensure(std::max<uint64_t>(input_elems, 1) * sizeof(double2));
-  std::memcpy(ctx->pin_in.p, input, input_elems * sizeof(double2));
-  QTNG_CUDA(cudaMemcpyAsync(ctx->A(), ctx->pin_in.p, input_elems * sizeof(double2),
-                            cudaMemcpyHostToDevice, ctx->stream));
+  ctx->pin_in.ensure(std::max<uint64_t>(input_elems, 1) * eb);
+  stage_input(hp, input, input_elems, ctx->pin_in.p);
+  QTNG_CUDA(cudaMemcpyAsync(ctx->arena.p, ctx->pin_in.p, input_elems * eb, cudaMemcpyHostToDevice,
+                            ctx->stream));
   upload_desc(ctx, hp, L, static_cast<char*>(ctx->desc.p));
-  DevProgram pr{static_cast<char*>(ctx->desc.p), L};
-  enqueue_program(ctx, hp, pr, ctx->A(), nullptr);
+  DevProgram pr{static_cast<char*>(ctx->desc.p), L, hp.c64};
+  enqueue_program(ctx, hp, pr, ctx->arena.p, nullptr);
   if (terms_host) {
     const size_t nb = (hp.lc_begin.size() - 1) * sizeof(double2);
     QTNG_CUDA(cudaMemcpyAsync(terms_host, pr.terms(), nb, cudaMemcpyDeviceToHost, ctx->stream));
@@ -644,15 +680,16 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
     std::vector<const WalkResult*> ptrs;
     for (const WalkResult& w : cs.walks) ptrs.push_back(&w);
     plan->hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
+    plan->hp.c64 = ctx->prec == 64;
     const HostPlan& hp = plan->hp;
     const DescLayout L = layout_of(hp);
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     plan->desc.ensure(L.total);
-    plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L};
+    plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L, hp.c64};
     upload_desc(ctx, hp, L, static_cast<char*>(plan->desc.p));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
-    plan->pin_gate.ensure(hp.input_elems * sizeof(double2));
+    plan->pin_gate.ensure(hp.input_elems * elem_bytes(hp));
     plan->pin_terms.ensure(std::max<size_t>(1, cs.walks.size()) * sizeof(double2));
     plan->lev_ev.resize(hp.levels.size() + 1);
     for (cudaEvent_t& e : plan->lev_ev) QTNG_CUDA(cudaEventCreate(&e));
@@ -686,7 +723,7 @@ qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* i
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     plan->desc.ensure(L.total);
-    plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L};
+    plan->prog = DevProgram{static_cast<char*>(plan->desc.p), L, false};
     upload_desc(ctx, hp, L, static_cast<char*>(plan->desc.p));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     plan->pin_gate.ensure(std::max<uint64_t>(input_elems, 1) * sizeof(double2));
@@ -710,13 +747,16 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     const HostPlan& hp = plan->hp;
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
-    ctx->ensure_arena(hp.arena_elems);
-    if (!plan->explicit_sched)
-      fill_gate_table(plan->p, gammas, betas, static_cast<double*>(plan->pin_gate.p));
-    QTNG_CUDA(cudaMemcpyAsync(ctx->A(), plan->pin_gate.p, hp.input_elems * sizeof(double2),
+    ctx->ensure_arena(hp.arena_elems, elem_bytes(hp));
+    if (!plan->explicit_sched) {
+      std::vector<double> table(2 * hp.input_elems);
+      fill_gate_table(plan->p, gammas, betas, table.data());
+      stage_input(hp, table.data(), hp.input_elems, plan->pin_gate.p);
+    }
+    QTNG_CUDA(cudaMemcpyAsync(ctx->arena.p, plan->pin_gate.p, hp.input_elems * elem_bytes(hp),
                               cudaMemcpyHostToDevice, ctx->stream));
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    enqueue_program(ctx, hp, plan->prog, ctx->A(), &plan->lev_ev, &plan->ker_ev);
+    enqueue_program(ctx, hp, plan->prog, ctx->arena.p, &plan->lev_ev, &plan->ker_ev);
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     const size_t nb = plan->edges.size() * sizeof(double2);
     QTNG_CUDA(cudaMemcpyAsync(plan->pin_terms.p, plan->prog.terms(), nb, cudaMemcpyDeviceToHost,
@@ -742,7 +782,7 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     if (device_ms) *device_ms = ms;
     const double* t = static_cast<const double*>(plan->pin_terms.p);
     if (terms) std::memcpy(terms, t, nb);
-    if (!plan->explicit_sched) check_terms(plan->edges, t);
+    if (!plan->explicit_sched) check_terms(plan->edges, t, imag_tol(hp.c64));
   });
 }
 
@@ -753,13 +793,13 @@ qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms) 
     const HostPlan& hp = plan->hp;
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
-    ctx->ensure_arena(hp.arena_elems);
+    ctx->ensure_arena(hp.arena_elems, elem_bytes(hp));
     if (!plan->graph || plan->graph_gen != ctx->arena_gen) {
       if (plan->graph) cudaGraphExecDestroy(plan->graph);
       plan->graph = nullptr;
       cudaGraph_t gr = nullptr;
       QTNG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      enqueue_program(ctx, hp, plan->prog, ctx->A(), nullptr);
+      enqueue_program(ctx, hp, plan->prog, ctx->arena.p, nullptr);
       QTNG_CUDA(cudaStreamEndCapture(ctx->stream, &gr));
       QTNG_CUDA(cudaGraphInstantiate(&plan->graph, gr, 0));
       cudaGraphDestroy(gr);
@@ -969,10 +1009,10 @@ qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* le
     qtng_ctx* ctx = plan->ctx;
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
-    ctx->ensure_arena(hp.arena_elems);
-    enqueue_level(ctx, hp.levels[level], level, plan->prog, ctx->A());  // warm-up
+    ctx->ensure_arena(hp.arena_elems, elem_bytes(hp));
+    enqueue_level(ctx, hp.levels[level], level, plan->prog, ctx->arena.p);  // warm-up
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    for (int i = 0; i < n_runs; ++i) enqueue_level(ctx, hp.levels[level], level, plan->prog, ctx->A());
+    for (int i = 0; i < n_runs; ++i) enqueue_level(ctx, hp.levels[level], level, plan->prog, ctx->arena.p);
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;
@@ -1009,7 +1049,8 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
     }
     std::vector<double> t(2 * cs.walks.size(), 0.0);
     if (!ok.empty()) {
-      const HostPlan hp = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
+      HostPlan hp = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
+      hp.c64 = ctx->prec == 64;
       std::vector<double> table(2 * hp.input_elems);
       fill_gate_table(p, gammas, betas, table.data());
       std::vector<double2> tt(ok.size());
@@ -1017,7 +1058,7 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
       QTNG_CUDA(cudaSetDevice(ctx->device));
       run_program_once(ctx, hp, table.data(), hp.input_elems, nullptr);
       ctx->pin_out.ensure(ok.size() * sizeof(double2));
-      DevProgram pr{static_cast<char*>(ctx->desc.p), layout_of(hp)};
+      DevProgram pr{static_cast<char*>(ctx->desc.p), layout_of(hp), hp.c64};
       QTNG_CUDA(cudaMemcpyAsync(ctx->pin_out.p, pr.terms(), ok.size() * sizeof(double2),
                                 cudaMemcpyDeviceToHost, ctx->stream));
       QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1029,7 +1070,7 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
     }
     for (size_t i = 0; i < cs.walks.size(); ++i) {
       const bool refused = cs.walks[i].fail_code != 0;
-      const bool complex_term = !refused && std::abs(t[2 * i + 1]) > 1e-8;
+      const bool complex_term = !refused && std::abs(t[2 * i + 1]) > imag_tol(ctx->prec == 64);
       if (refused || complex_term) {
         const std::string what = refused ? cs.walks[i].fail_msg
                                          : "edge term has non-real value: imag = " +

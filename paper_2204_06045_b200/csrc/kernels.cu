@@ -30,7 +30,20 @@
 
 #include <cstdint>
 
+#ifndef QTNG_C64
+#define QTNG_C64 0  // 1: the complex64 build of this file (namespace qtng::c64)
+#endif
+
 namespace qtng {
+namespace QTNG_PREC_NS {
+
+#if QTNG_C64
+using V = float2;  // complex64 mode: results within the north_star's 1e-5
+using R = float;
+#else
+using V = double2;  // complex128: bit-identical to the reference's naive backend
+using R = double;
+#endif
 
 namespace {
 
@@ -39,23 +52,28 @@ constexpr int kWarpsPerCta = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSmemOps = 4096;  // item_begin entries cached in shared memory
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ V mkv(R x, R y) { V v; v.x = x; v.y = y; return v; }
+
+__device__ __forceinline__ V cmul(V a, V b) {
   // (a.x*b.x - a.y*b.y, a.x*b.y + a.y*b.x), every product rounded.
-  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+  return mkv(rsub(rmul(a.x, b.x), rmul(a.y, b.y)), radd(rmul(a.x, b.y), rmul(a.y, b.x)));
 }
 
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
-  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
-}
+__device__ __forceinline__ V cadd(V a, V b) { return mkv(radd(a.x, b.x), radd(a.y, b.y)); }
 
-__device__ __forceinline__ double2 ld(const double2* p) { return __ldg(p); }
+__device__ __forceinline__ V ld(const V* p) { return __ldg(p); }
 
 // Product over the T operands of one summed assignment (left fold, member order).
 template <int T>
-__device__ __forceinline__ double2 chain(const double2* const* base, const uint32_t* off,
+__device__ __forceinline__ V chain(const V* const* base, const uint32_t* off,
                                          uint32_t add) {
-  double2 p = ld(base[0] + off[0] + add);
+  V p = ld(base[0] + off[0] + add);
 #pragma unroll
   for (int t = 1; t < T; ++t) p = cmul(p, ld(base[t] + off[t] + add));
   return p;
@@ -66,7 +84,7 @@ __device__ __forceinline__ double2 chain(const double2* const* base, const uint3
 template <int T, int NSM, int K>
 __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
                                          const DevTensor* __restrict__ trefs,
-                                         double2* __restrict__ arena, int lane,
+                                         V* __restrict__ arena, int lane,
                                          DevTensor* slot) {
   const int cb = op.cb;
   const uint64_t kbase = static_cast<uint64_t>(chunk) << cb;
@@ -81,7 +99,7 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
     if (lane < 3 * T) dst4[lane] = __ldg(src4 + lane);
     __syncwarp();
   }
-  const double2* base[T];
+  const V* base[T];
   uint32_t lo[T], hi[T], sa[T], sb[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) {
@@ -115,9 +133,9 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
   }
   __syncwarp();  // the slot is rewritten by the warp's next item
   const int rows = cb > 5 ? 1 << (cb - 5) : 1;
-  double2* out = arena + op.out + kbase + my;
+  V* out = arena + op.out + kbase + my;
   if (NSM != 2) {
-    double2 g0 = make_double2(0.0, 0.0), g1 = g0;
+    V g0 = mkv(0.0, 0.0), g1 = g0;
     if (K == 1) {  // member 0 has no row bit: one load per item, both summed values
       const uint32_t o = lo[0] + __shfl_sync(kFull, hi[0], 0);
       g0 = ld(base[0] + o);
@@ -132,14 +150,14 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
         o0[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
         o1[t] = lo[t] + __shfl_sync(kFull, hi[t], two ? e + 1 : e);
       }
-      double2 r0, r1;
+      V r0, r1;
       if (NSM == 0) {
         r0 = chain<T>(base, o0, 0);
         r1 = chain<T>(base, o1, 0);
       } else {
         // s = 0 and s = 1 of both rows; a row-invariant member 0 (K == 1) was
         // loaded once for the whole item
-        double2 a0, b0, a1, b1;
+        V a0, b0, a1, b1;
         if (K == 1) {
           a0 = a1 = g0;
           b0 = b1 = g1;
@@ -151,8 +169,8 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
         }
 #pragma unroll
         for (int t = 1; t < T; ++t) {
-          const double2 xa0 = ld(base[t] + o0[t]), xb0 = ld(base[t] + o0[t] + sa[t]);
-          const double2 xa1 = ld(base[t] + o1[t]), xb1 = ld(base[t] + o1[t] + sa[t]);
+          const V xa0 = ld(base[t] + o0[t]), xb0 = ld(base[t] + o0[t] + sa[t]);
+          const V xa1 = ld(base[t] + o1[t]), xb1 = ld(base[t] + o1[t] + sa[t]);
           a0 = cmul(a0, xa0);
           b0 = cmul(b0, xb0);
           a1 = cmul(a1, xa1);
@@ -174,7 +192,7 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
       uint32_t off[T];
 #pragma unroll
       for (int t = 0; t < T; ++t) off[t] = lo[t] + __shfl_sync(kFull, hi[t], e);
-      double2 acc = make_double2(0.0, 0.0);
+      V acc = mkv(0.0, 0.0);
       bool first = true;
       for (int sh = 0; sh < n_hi; ++sh) {
         uint32_t offh[T];
@@ -184,7 +202,7 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
           uint32_t o[T];
 #pragma unroll
           for (int t = 0; t < T; ++t) o[t] = offh[t] + __shfl_sync(kFull, sa[t], sl);
-          const double2 p = chain<T>(base, o, 0);
+          const V p = chain<T>(base, o, 0);
           acc = first ? p : cadd(acc, p);
           first = false;
         }
@@ -197,7 +215,7 @@ __device__ __forceinline__ void run_item(const DevOp& op, uint32_t chunk,
 template <int T>
 __device__ __forceinline__ void dispatch_ns(const DevOp& op, uint32_t chunk,
                                             const DevTensor* __restrict__ trefs,
-                                            double2* __restrict__ arena, int lane,
+                                            V* __restrict__ arena, int lane,
                                             DevTensor* slot) {
   if (op.ns == 1) {
     if (T >= 2 && op.inv0) run_item<T, 1, 1>(op, chunk, trefs, arena, lane, slot);
@@ -220,7 +238,7 @@ template <int MAXT>
 #endif
 __global__ void __launch_bounds__(kThreads, MAXT <= 2 ? QTNG_MINB_T2 : (MAXT <= 4 ? QTNG_MINB_T4 : 2))
 level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
-             const DevTensor* __restrict__ trefs, double2* __restrict__ arena,
+             const DevTensor* __restrict__ trefs, V* __restrict__ arena,
              uint32_t op_count, uint32_t items) {
   __shared__ DevTensor slots[kWarpsPerCta][MAXT];
   __shared__ uint32_t sbeg[kSmemOps];
@@ -273,7 +291,7 @@ __device__ __forceinline__ uint32_t insert_zero(uint32_t x, uint32_t q) {
 template <int LEAD>
 __device__ __forceinline__ void run_outer(const DevOp& op, uint32_t chunk,
                                           const DevTensor* __restrict__ trefs,
-                                          double2* __restrict__ arena, int lane, DevTensor* slot) {
+                                          V* __restrict__ arena, int lane, DevTensor* slot) {
   constexpr int T = LEAD + 2;
   const int cb = op.cb;  // >= 7 by construction
   const uint64_t kbase = static_cast<uint64_t>(chunk) << cb;
@@ -285,7 +303,7 @@ __device__ __forceinline__ void run_outer(const DevOp& op, uint32_t chunk,
     if (lane < 3 * T) dst4[lane] = __ldg(src4 + lane);
     __syncwarp();
   }
-  const double2* base[T];
+  const V* base[T];
   uint32_t lo[T], hi[T], sa[T], d0[T], d1[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) {
@@ -311,29 +329,29 @@ __device__ __forceinline__ void run_outer(const DevOp& op, uint32_t chunk,
   }
   __syncwarp();
   // prefix of the row-invariant leading members, both summed values
-  double2 pre0 = make_double2(1.0, 0.0), pre1 = pre0;
+  V pre0 = mkv(1.0, 0.0), pre1 = pre0;
 #pragma unroll
   for (int t = 0; t < LEAD; ++t) {
-    const double2* p = base[t] + lo[t] + __shfl_sync(kFull, hi[t], 0);
-    const double2 x = ld(p), y = ld(p + sa[t]);
+    const V* p = base[t] + lo[t] + __shfl_sync(kFull, hi[t], 0);
+    const V x = ld(p), y = ld(p + sa[t]);
     pre0 = t == 0 ? x : cmul(pre0, x);
     pre1 = t == 0 ? y : cmul(pre1, y);
   }
   const uint32_t q0 = r0 - 5u, q1 = r1 - 5u;
   const uint32_t qa = q0 < q1 ? q0 : q1, qb = q0 < q1 ? q1 : q0;
   const int steps = 1 << (cb - 7);
-  double2* out = arena + op.out + kbase + lane;
+  V* out = arena + op.out + kbase + lane;
   constexpr int A = LEAD, B = LEAD + 1;
   for (int it = 0; it < steps; ++it) {
     const uint32_t e = insert_zero(insert_zero(static_cast<uint32_t>(it), qa), qb);
-    const double2* pa = base[A] + lo[A] + __shfl_sync(kFull, hi[A], e);
-    const double2* pb = base[B] + lo[B] + __shfl_sync(kFull, hi[B], e);
-    const double2 a00 = ld(pa), a01 = ld(pa + sa[A]);                   // rb0 = 0
-    const double2 a10 = ld(pa + d0[A]), a11 = ld(pa + d0[A] + sa[A]);   // rb0 = 1
-    const double2 b00 = ld(pb), b01 = ld(pb + sa[B]);                   // rb1 = 0
-    const double2 b10 = ld(pb + d1[B]), b11 = ld(pb + d1[B] + sa[B]);   // rb1 = 1
-    const double2 p00 = LEAD ? cmul(pre0, a00) : a00, p01 = LEAD ? cmul(pre1, a01) : a01;
-    const double2 p10 = LEAD ? cmul(pre0, a10) : a10, p11 = LEAD ? cmul(pre1, a11) : a11;
+    const V* pa = base[A] + lo[A] + __shfl_sync(kFull, hi[A], e);
+    const V* pb = base[B] + lo[B] + __shfl_sync(kFull, hi[B], e);
+    const V a00 = ld(pa), a01 = ld(pa + sa[A]);                   // rb0 = 0
+    const V a10 = ld(pa + d0[A]), a11 = ld(pa + d0[A] + sa[A]);   // rb0 = 1
+    const V b00 = ld(pb), b01 = ld(pb + sa[B]);                   // rb1 = 0
+    const V b10 = ld(pb + d1[B]), b11 = ld(pb + d1[B] + sa[B]);   // rb1 = 1
+    const V p00 = LEAD ? cmul(pre0, a00) : a00, p01 = LEAD ? cmul(pre1, a01) : a01;
+    const V p10 = LEAD ? cmul(pre0, a10) : a10, p11 = LEAD ? cmul(pre1, a11) : a11;
     const uint64_t r00 = static_cast<uint64_t>(e) << 5;
     const uint64_t ra = static_cast<uint64_t>(1u << q0) << 5, rb = static_cast<uint64_t>(1u << q1) << 5;
     out[r00] = cadd(cmul(p00, b00), cmul(p01, b01));
@@ -345,7 +363,7 @@ __device__ __forceinline__ void run_outer(const DevOp& op, uint32_t chunk,
 
 __global__ void __launch_bounds__(kThreads, 2)
 outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
-             const DevTensor* __restrict__ trefs, double2* __restrict__ arena,
+             const DevTensor* __restrict__ trefs, V* __restrict__ arena,
              uint32_t op_count, uint32_t items) {
   __shared__ DevTensor slots[kWarpsPerCta][4];
   __shared__ uint32_t sbeg[kSmemOps];
@@ -442,18 +460,18 @@ __global__ void seg_prep_kernel(const DevSeg* __restrict__ segs, uint32_t n_segs
 struct ChainWarp {
   uint32_t toff[kSegMaxOps];             // tile part of each operand's offset
   DevStage st[kSegMaxStages];
-  double2 ptab[kSegMaxStages][8];        // tabulated side products P_i(s_i, u0, u1) of this tile
+  V ptab[kSegMaxStages][8];        // tabulated side products P_i(s_i, u0, u1) of this tile
   uint8_t preal[kSegMaxStages];          // 1: P_i is a real scalar (scale instead of multiply)
-  double2 acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
+  V acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
 };
 
 // (r, 0) * y and p * (r, 0): equal to cmul up to the sign of an exact zero.
-__device__ __forceinline__ double2 rscale(double r, double2 y) {
-  return make_double2(__dmul_rn(r, y.x), __dmul_rn(r, y.y));
+__device__ __forceinline__ V rscale(R r, V y) {
+  return mkv(rmul(r, y.x), rmul(r, y.y));
 }
 
 // One left-fold step p * y where either factor may be a real scalar (r, 0).
-__device__ __forceinline__ double2 fmul(double2 p, bool p_real, double2 y, bool y_real) {
+__device__ __forceinline__ V fmul(V p, bool p_real, V y, bool y_real) {
   if (y_real) return rscale(y.x, p);
   if (p_real) return rscale(p.x, y);
   return cmul(p, y);
@@ -461,11 +479,11 @@ __device__ __forceinline__ double2 fmul(double2 p, bool p_real, double2 y, bool 
 
 // Side-member product P_i (left fold of members [op0, op0+m)) at digit
 // assignment j; m >= 1.  *real: P is a real scalar (r, 0).
-__device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
-                                              const double2* __restrict__ arena, int op0, int m,
+__device__ __forceinline__ V chain_side(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                              const V* __restrict__ arena, int op0, int m,
                                               uint32_t j, int lane, bool* real) {
   const uint32_t jl = j & 15u, jh = j >> 4;
-  double2 p = make_double2(0.0, 0.0);
+  V p = mkv(0.0, 0.0);
   bool pr = false;
 #pragma unroll
   for (int t = 0; t < kSegMaxNt - 1; ++t) {  // unrolled: loads of independent terms overlap
@@ -473,7 +491,7 @@ __device__ __forceinline__ double2 chain_side(const ChainWarp& cw, const SegOpTa
     const int op = op0 + t;
     const SegOpTab* tb = tab + op;
     const bool xr = __ldg(&tb->kind) == kTensorRealScalar;
-    const double2 x = xr ? make_double2(__ldg(&(arena + __ldg(&tb->off))->x), 0.0)
+    const V x = xr ? mkv(__ldg(&(arena + __ldg(&tb->off))->x), 0.0)
                          : ld(arena + __ldg(&tb->off) +
                               (cw.toff[op] + __ldg(&tb->llane[lane]) + __ldg(&tb->dlo[jl]) +
                                __ldg(&tb->dhi[jh])));
@@ -502,19 +520,19 @@ __device__ __forceinline__ uint32_t ptab_bit(uint8_t c, uint32_t j, int lane) {
 }
 
 // term of stage i = k + 2 (DevStage st) at digit assignment j: P_i(j) * v, or v.
-__device__ __forceinline__ double2 chain_term(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
-                                              const double2* __restrict__ arena, const DevStage st,
-                                              int k, uint32_t j, double2 v, int lane) {
+__device__ __forceinline__ V chain_term(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                              const V* __restrict__ arena, const DevStage st,
+                                              int k, uint32_t j, V v, int lane) {
   if (QTNG_SEG_PTAB && st.ptab) {
     const uint32_t idx = ((j >> k) & 1u) | (ptab_bit(st.u[0], j, lane) << 1) |
                          (ptab_bit(st.u[1], j, lane) << 2);
-    const double2 p = cw.ptab[k + 1][idx];
+    const V p = cw.ptab[k + 1][idx];
     return cw.preal[k + 1] ? rscale(p.x, v) : cmul(p, v);
   }
   const int m = st.nt - 1;
   if (!m) return v;
   bool real;
-  const double2 p = chain_side(cw, tab, arena, st.op0, m, j, lane, &real);
+  const V p = chain_side(cw, tab, arena, st.op0, m, j, lane, &real);
   return real ? rscale(p.x, v) : cmul(p, v);
 }
 
@@ -523,16 +541,16 @@ __device__ __forceinline__ double2 chain_term(const ChainWarp& cw, const SegOpTa
 // stage-1 products in flight), then the climb above each group.
 template <int NT, int NS, int U, int K0>
 __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __restrict__ tab,
-                                           const DevSeg& sg, double2* __restrict__ arena,
+                                           const DevSeg& sg, V* __restrict__ arena,
                                            uint32_t tile, int lane) {
   constexpr int G = 1 << U;
   const int L = sg.nst;
   const uint32_t nj = 1u << (L - 1);
-  const double2* B[NT];
+  const V* B[NT];
   uint32_t o[NT], sdl[NT], d0[NT], d1[NT];
   // K0: member 0 is a real scalar r (the |+> state on the summed var): the
   // first product (r, 0) * M1 becomes a scale, and member 0 is not gathered
-  const double r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : 0.0;
+  const R r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : 0.0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     B[t] = arena + __ldg(&tab[t].off);
@@ -549,17 +567,17 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
 #pragma unroll
       for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t] + d1[t];
     }
-    double2 v[G];
+    V v[G];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
       uint32_t oq[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t) oq[t] = o[t] + ((q & 1) ? d0[t] : 0u) + ((q & 2) ? d1[t] : 0u);
-      double2 x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
+      V x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
 #pragma unroll
       for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
       if (NS) {
-        double2 p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
+        V p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
 #pragma unroll
         for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
         x = cadd(x, p);
@@ -567,10 +585,10 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
       v[q] = x;
     }
     // stage 2 over bit 0, stage 3 over bit 1 (U == 2)
-    double2 x = cadd(chain_term(cw, tab, arena, st2, 0, j, v[0], lane),
+    V x = cadd(chain_term(cw, tab, arena, st2, 0, j, v[0], lane),
                      chain_term(cw, tab, arena, st2, 0, j | 1u, v[1], lane));
     if (U > 1) {
-      const double2 y = cadd(chain_term(cw, tab, arena, st2, 0, j | 2u, v[2], lane),
+      const V y = cadd(chain_term(cw, tab, arena, st2, 0, j | 2u, v[2], lane),
                              chain_term(cw, tab, arena, st2, 0, j | 3u, v[3], lane));
       x = cadd(chain_term(cw, tab, arena, st3, 1, j, x, lane),
                chain_term(cw, tab, arena, st3, 1, j | 2u, y, lane));
@@ -579,7 +597,7 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
     const uint32_t jj = j | (G - 1);
     bool carry = true;
     for (int k = U; k + 2 <= L; ++k) {
-      const double2 term = chain_term(cw, tab, arena, cw.st[k + 1], k, jj, x, lane);
+      const V term = chain_term(cw, tab, arena, cw.st[k + 1], k, jj, x, lane);
       if (!((jj >> k) & 1u)) {
         cw.acc[k - 1][lane] = term;
         carry = false;
@@ -600,18 +618,18 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
 // then the climb parks s_i = 0 terms in shared memory.
 template <int NT, int NS, int K0>
 __device__ __noinline__ void chain_tile_lanes(ChainWarp& cw, const SegOpTab* __restrict__ tab,
-                                           const DevSeg& sg, double2* __restrict__ arena,
+                                           const DevSeg& sg, V* __restrict__ arena,
                                            uint32_t tile, int lane) {
   const int L = sg.nst, J = L - 1, cy = sg.cy;
   const int nld = min(kSegYBits - cy, J);
   const uint32_t ldig = (static_cast<uint32_t>(lane) >> cy) & ((1u << nld) - 1u);
   const uint32_t nloop = 1u << (J - nld);
   const int G = nloop > 1 ? 2 : 1;
-  const double2* B[NT];
+  const V* B[NT];
   uint32_t o[NT], sdl[NT], d0[NT], sld[NT];
   // K0: member 0 is a real scalar r (the |+> state on the summed var): the
   // first product (r, 0) * M1 becomes a scale, and member 0 is not gathered
-  const double r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : 0.0;
+  const R r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : 0.0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     const SegOpTab* tb = tab + t;
@@ -633,18 +651,18 @@ __device__ __noinline__ void chain_tile_lanes(ChainWarp& cw, const SegOpTab* __r
 #pragma unroll
       for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + sld[t] + d0[t];
     }
-    double2 v[2];
+    V v[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       if (q >= G) break;
       uint32_t oq[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t) oq[t] = o[t] + (q ? d0[t] : 0u);
-      double2 x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
+      V x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
 #pragma unroll
       for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
       if (NS) {
-        double2 p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
+        V p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
 #pragma unroll
         for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
         x = cadd(x, p);
@@ -652,14 +670,14 @@ __device__ __noinline__ void chain_tile_lanes(ChainWarp& cw, const SegOpTab* __r
       // lane-digit stages: combine with the sibling lane
       const uint32_t fj = ((j + q) << nld) | ldig;
       for (int k = 0; k < nld; ++k) {
-        const double2 t = chain_term(cw, tab, arena, cw.st[k + 1], k, fj, x, lane);
-        const double2 u = make_double2(__shfl_xor_sync(kFull, t.x, 1 << (cy + k)),
+        const V t = chain_term(cw, tab, arena, cw.st[k + 1], k, fj, x, lane);
+        const V u = mkv(__shfl_xor_sync(kFull, t.x, 1 << (cy + k)),
                                        __shfl_xor_sync(kFull, t.y, 1 << (cy + k)));
         x = cadd(t, u);
       }
       v[q] = x;
     }
-    double2 x = v[0];
+    V x = v[0];
     if (G > 1) {  // the pair's stage (digit nld) in registers
       const uint32_t f0 = (j << nld) | ldig;
       x = cadd(chain_term(cw, tab, arena, cw.st[nld + 1], nld, f0, v[0], lane),
@@ -669,7 +687,7 @@ __device__ __noinline__ void chain_tile_lanes(ChainWarp& cw, const SegOpTab* __r
     const uint32_t jj = ((j | (G - 1)) << nld) | ldig;
     bool carry = true;
     for (int k = nld + 1; k + 2 <= L; ++k) {
-      const double2 term = chain_term(cw, tab, arena, cw.st[k + 1], k, jj, x, lane);
+      const V term = chain_term(cw, tab, arena, cw.st[k + 1], k, jj, x, lane);
       if (!((jj >> k) & 1u)) {
         cw.acc[k - 1][lane] = term;
         carry = false;
@@ -684,7 +702,7 @@ __device__ __noinline__ void chain_tile_lanes(ChainWarp& cw, const SegOpTab* __r
 
 template <int NT, int NS>
 __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __restrict__ tab,
-                                             const DevSeg& sg, double2* __restrict__ arena,
+                                             const DevSeg& sg, V* __restrict__ arena,
                                              uint32_t tile, int lane) {
   const bool k0 = NT >= 2 && __ldg(&tab[0].kind) == kTensorRealScalar;
   if (sg.cy < kSegYBits) {  // chain tails: digits on the idle lanes
@@ -702,7 +720,7 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
 // kept out of line so the hot loop's registers are not spilled for it.
 __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
                                               const DevTensor* __restrict__ trefs,
-                                              const double2* __restrict__ arena, uint32_t tile,
+                                              const V* __restrict__ arena, uint32_t tile,
                                               int lane) {
   for (int base = 8; base < 8 * sg.nst; base += 32) {
     const int i = (base + lane) >> 3, e = (base + lane) & 7;
@@ -715,7 +733,7 @@ __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
         if (c >= kTileSrc && c < kSumSrc) return (tile >> (c - kTileSrc)) & 1u;
         return (e >> (1 + w)) & 1;
       };
-      double2 p = make_double2(0.0, 0.0);
+      V p = mkv(0.0, 0.0);
       bool pr = false;
       for (int t = 0; t < st.nt - 1; ++t) {
         const DevTensor* d = trefs + sg.tref + st.op0 + t;
@@ -723,7 +741,7 @@ __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
         uint32_t o = 0;
         for (int ax = 0; ax < rank; ++ax) o |= val(d->src[ax]) << (rank - 1 - ax);
         const bool xr = d->kind == kTensorRealScalar;
-        const double2 x = xr ? make_double2(__ldg(&(arena + d->off)->x), 0.0) : ld(arena + d->off + o);
+        const V x = xr ? mkv(__ldg(&(arena + d->off)->x), 0.0) : ld(arena + d->off + o);
         if (t == 0) {
           p = x;
           pr = xr;
@@ -743,7 +761,7 @@ __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
 __global__ void __launch_bounds__(32, QTNG_SEG_MINB)
 seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
            const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
-           const SegOpTab* __restrict__ segtab, double2* __restrict__ arena, uint32_t seg_count,
+           const SegOpTab* __restrict__ segtab, V* __restrict__ arena, uint32_t seg_count,
            uint32_t items, uint32_t* ctr) {
   __shared__ ChainWarp cw;
   const int lane = threadIdx.x;
@@ -837,13 +855,20 @@ int seg_grid(uint32_t items) {
   return static_cast<int>(items < static_cast<uint32_t>(cap) ? (items > 0 ? items : 1) : cap);
 }
 
+// Per lightcone: e_jk = prod of its scalar results in production order
+// (complex128 arithmetic also for complex64 plans).
 __global__ void final_kernel(const uint64_t* __restrict__ scalar_off,
                              const uint32_t* __restrict__ lc_begin, int n_lc,
-                             const double2* __restrict__ arena, double2* __restrict__ terms) {
+                             const V* __restrict__ arena, double2* __restrict__ terms) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_lc) return;
   double2 s = make_double2(1.0, 0.0);  // report.scalar = 1 (engine.cpp:253)
-  for (uint32_t k = lc_begin[i]; k < lc_begin[i + 1]; ++k) s = cmul(s, arena[scalar_off[k]]);
+  for (uint32_t k = lc_begin[i]; k < lc_begin[i + 1]; ++k) {
+    const V a = arena[scalar_off[k]];
+    const double2 b = make_double2(static_cast<double>(a.x), static_cast<double>(a.y));
+    s = make_double2(__dsub_rn(__dmul_rn(s.x, b.x), __dmul_rn(s.y, b.y)),
+                     __dadd_rn(__dmul_rn(s.x, b.y), __dmul_rn(s.y, b.x)));
+  }
   terms[i] = s;
 }
 
@@ -883,8 +908,9 @@ int outer_grid(uint32_t items) {
 }  // namespace
 
 cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
-                         const DevTensor* trefs, double2* arena, const LevelLaunch& lv) {
+                         const DevTensor* trefs, void* arena_v, const LevelLaunch& lv) {
   if (lv.outer_items == 0) return cudaSuccess;
+  V* arena = static_cast<V*>(arena_v);
   const uint32_t first = lv.op_begin + lv.op_count;
   outer_kernel<<<outer_grid(lv.outer_items), kThreads, 0, s>>>(ops + first, ibeg + first, trefs,
                                                                arena, lv.outer_count,
@@ -901,8 +927,9 @@ cudaError_t launch_seg_prep(cudaStream_t s, const DevSeg* segs, uint32_t n_segs,
 
 cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
                         const DevStage* stages, const DevTensor* trefs, const SegOpTab* segtab,
-                        double2* arena, uint32_t* ctr, const LevelLaunch& lv) {
+                        void* arena_v, uint32_t* ctr, const LevelLaunch& lv) {
   if (lv.seg_items == 0) return cudaSuccess;
+  V* arena = static_cast<V*>(arena_v);
   seg_kernel<<<seg_grid(lv.seg_items), 32, 0, s>>>(
       segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, trefs, segtab, arena, lv.seg_count,
       lv.seg_items, ctr);
@@ -914,8 +941,9 @@ int level_grid(uint32_t items) { return grid_for<8>(items); }
 int resident_warps() { return resident_ctas<4>() * kWarpsPerCta; }
 
 cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
-                         const DevTensor* trefs, double2* arena, const LevelLaunch& lv) {
+                         const DevTensor* trefs, void* arena_v, const LevelLaunch& lv) {
   if (lv.items == 0) return cudaSuccess;
+  V* arena = static_cast<V*>(arena_v);
   const DevOp* o = ops + lv.op_begin;
   const uint32_t* b = ibeg + lv.op_begin;
   if (lv.max_nt <= 2)
@@ -928,10 +956,12 @@ cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
 }
 
 cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint32_t* lc_begin,
-                         int n_lc, const double2* arena, double2* terms) {
+                         int n_lc, const void* arena_v, double2* terms) {
   if (n_lc <= 0) return cudaSuccess;
+  const V* arena = static_cast<const V*>(arena_v);
   final_kernel<<<(n_lc + 127) / 128, 128, 0, s>>>(scalar_off, lc_begin, n_lc, arena, terms);
   return cudaGetLastError();
 }
 
+}  // namespace QTNG_PREC_NS
 }  // namespace qtng

@@ -25,6 +25,7 @@ struct HostPlan {
   // per unit sum of its materialised inputs + its output
   double dev_bytes = 0;
   uint64_t n_fused_ops = 0;            // ops evaluated inside segments
+  bool c64 = false;                    // complex64 arena/kernels (set by the caller)
   double fp64_ops = 0;                 // the reference's FP64 mul/add count (all ops)
   double seg_fp64_ops = 0;             // ... of the ops inside segments
   double single_alg_bytes = 0;         // B_alg of the single (level/outer kernel) ops
