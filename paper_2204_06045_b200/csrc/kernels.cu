@@ -462,6 +462,11 @@ struct ChainWarp {
   DevStage st[kSegMaxStages];
   V ptab[kSegMaxStages][8];        // tabulated side products P_i(s_i, u0, u1) of this tile
   uint8_t preal[kSegMaxStages];          // 1: P_i is a real scalar (scale instead of multiply)
+  // per stage: bits 0-1 mode (0 no side member, 1 table, 2 real table, 3
+  // gathered), bits 8-12 / 13 and 16-20 / 21: digit position / valid of the
+  // table index bits 1 and 2
+  uint32_t sdesc[kSegMaxStages];
+  uint8_t slane[kSegMaxStages][32];      // per lane: the lane bits of the table index
   V acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
 };
 
@@ -507,30 +512,28 @@ __device__ __forceinline__ V chain_side(const ChainWarp& cw, const SegOpTab* __r
   return p;
 }
 
+#ifndef QTNG_SEG_U2_MAXNT
+#define QTNG_SEG_U2_MAXNT 0  // heads with <= this many members walk digits in fours
+#endif
 #ifndef QTNG_SEG_PTAB
 #define QTNG_SEG_PTAB 1  // tabulated side products in the climb
 #endif
-
-// Index bit of a tabulated side product from var code c (lane / digit bit;
-// tile bits are fixed per tile and folded into the table).
-__device__ __forceinline__ uint32_t ptab_bit(uint8_t c, uint32_t j, int lane) {
-  if (c < kLaneSrcEnd) return (static_cast<uint32_t>(lane) >> c) & 1u;
-  if (c >= kJSrc && c < kTileSrc) return (j >> (c - kJSrc)) & 1u;
-  return 0u;
-}
 
 // term of stage i = k + 2 (DevStage st) at digit assignment j: P_i(j) * v, or v.
 __device__ __forceinline__ V chain_term(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                               const V* __restrict__ arena, const DevStage st,
                                               int k, uint32_t j, V v, int lane) {
-  if (QTNG_SEG_PTAB && st.ptab) {
-    const uint32_t idx = ((j >> k) & 1u) | (ptab_bit(st.u[0], j, lane) << 1) |
-                         (ptab_bit(st.u[1], j, lane) << 2);
+  const uint32_t d = cw.sdesc[k + 1];
+  const uint32_t mode = d & 3u;
+  if (mode == 0) return v;
+  if (mode != 3) {
+    const uint32_t idx = cw.slane[k + 1][lane] | ((j >> k) & 1u) |
+                         (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
+                         (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
     const V p = cw.ptab[k + 1][idx];
-    return cw.preal[k + 1] ? rscale(p.x, v) : cmul(p, v);
+    return mode == 2 ? rscale(p.x, v) : cmul(p, v);
   }
   const int m = st.nt - 1;
-  if (!m) return v;
   bool real;
   const V p = chain_side(cw, tab, arena, st.op0, m, j, lane, &real);
   return real ? rscale(p.x, v) : cmul(p, v);
@@ -710,6 +713,12 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
     else chain_tile_lanes<NT, NS, 0>(cw, tab, sg, arena, tile, lane);
     return;
   }
+  constexpr int U = NT <= QTNG_SEG_U2_MAXNT ? 2 : 1;  // groups of 2^U digit values
+  if (U == 2 && sg.nst >= 3) {
+    if (k0) chain_tile<NT, NS, U, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+    else chain_tile<NT, NS, U, 0>(cw, tab, sg, arena, tile, lane);
+    return;
+  }
   if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
   else chain_tile<NT, NS, 1, 0>(cw, tab, sg, arena, tile, lane);
 }
@@ -797,6 +806,22 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
           cw.preal[lane] = real ? 1 : 0;
           for (int w = 0; w < 2; ++w)
             tile_dep |= st.ptab && st.u[w] >= kTileSrc && st.u[w] < kSumSrc;
+          const uint32_t mode = st.nt <= 1 ? 0u : (QTNG_SEG_PTAB && st.ptab ? (real ? 2u : 1u) : 3u);
+          uint32_t d = mode;
+          for (int w = 0; w < 2; ++w)
+            if (mode == 1u || mode == 2u) {
+              const uint32_t c = st.u[w];
+              if (c >= kJSrc && c < kTileSrc) d |= ((c - kJSrc) | 32u) << (8 + 8 * w);
+            }
+          cw.sdesc[lane] = d;
+        }
+        __syncwarp();
+        for (int i = 0; i < sg.nst; ++i) {  // lane bits of each table index
+          const DevStage st = cw.st[i];
+          uint32_t b = 0;
+          for (int w = 0; w < 2; ++w)
+            if (st.u[w] < kLaneSrcEnd) b |= ((static_cast<uint32_t>(lane) >> st.u[w]) & 1u) << (1 + w);
+          cw.slane[i][lane] = static_cast<uint8_t>(b);
         }
         // the side-product tables depend on the tile only through tile-bit u's
         ptab_tile = __any_sync(kFull, tile_dep);
