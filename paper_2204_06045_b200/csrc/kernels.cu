@@ -242,7 +242,10 @@ level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
              uint32_t op_count, uint32_t items) {
   __shared__ DevTensor slots[kWarpsPerCta][MAXT];
   __shared__ uint32_t sbeg[kSmemOps];
-  const bool cached = op_count <= kSmemOps;
+  // cache the item table in shared memory only when each warp will look it
+  // up several times (small levels: a couple of binary searches in L1/L2 are
+  // cheaper than every CTA copying the whole table)
+  const bool cached = op_count <= kSmemOps && items >= 4u * gridDim.x * kWarpsPerCta;
   if (cached)
     for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
   __syncthreads();
@@ -367,7 +370,10 @@ outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
              uint32_t op_count, uint32_t items) {
   __shared__ DevTensor slots[kWarpsPerCta][4];
   __shared__ uint32_t sbeg[kSmemOps];
-  const bool cached = op_count <= kSmemOps;
+  // cache the item table in shared memory only when each warp will look it
+  // up several times (small levels: a couple of binary searches in L1/L2 are
+  // cheaper than every CTA copying the whole table)
+  const bool cached = op_count <= kSmemOps && items >= 4u * gridDim.x * kWarpsPerCta;
   if (cached)
     for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
   __syncthreads();
