@@ -7,6 +7,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 #include <memory>
@@ -33,6 +36,28 @@ thread_local std::string g_err;
     if (e_ != cudaSuccess)                                                               \
       throw Error(kCuda, std::string(#call) + ": " + cudaGetErrorString(e_));            \
   } while (0)
+
+// QTNG_TIMING=1: host phase times of the one-shot calls on stderr (tuning aid).
+struct PhaseTimer {
+  const char* name;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(const char* n) : name(n) {
+    static const bool enabled = [] {
+      const char* v = std::getenv("QTNG_TIMING");
+      return v && v[0] == '1';
+    }();
+    on = enabled;
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* phase) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "%s %s %.3f ms\n", name, phase,
+                 std::chrono::duration<double>(now - t).count() * 1e3);
+    t = now;
+  }
+};
 
 template <class F>
 qtng_status guarded(F&& f) {
@@ -1034,7 +1059,9 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
     validate_angles(p, gammas, betas);
     const Graph g = graph_from(n, m, edges);
     const std::vector<int> s = selection(m, n_sel, sel);
+    PhaseTimer tm("qtng_energy");
     ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, s);
+    tm.mark("schedules+walks");
     // cap refusals surface per edge, the first in edge order wins (engine.cpp:543-546)
     std::vector<const WalkResult*> ok;
     std::vector<int> ok_idx;
@@ -1051,17 +1078,19 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
     if (!ok.empty()) {
       HostPlan hp = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
       hp.c64 = ctx->prec == 64;
+      tm.mark("build_plan");
       std::vector<double> table(2 * hp.input_elems);
       fill_gate_table(p, gammas, betas, table.data());
-      std::vector<double2> tt(ok.size());
       std::lock_guard<std::mutex> lk(ctx->mu);
       QTNG_CUDA(cudaSetDevice(ctx->device));
       run_program_once(ctx, hp, table.data(), hp.input_elems, nullptr);
+      tm.mark("upload+enqueue");
       ctx->pin_out.ensure(ok.size() * sizeof(double2));
       DevProgram pr{static_cast<char*>(ctx->desc.p), layout_of(hp), hp.c64};
       QTNG_CUDA(cudaMemcpyAsync(ctx->pin_out.p, pr.terms(), ok.size() * sizeof(double2),
                                 cudaMemcpyDeviceToHost, ctx->stream));
       QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+      tm.mark("device+d2h");
       const double* o = static_cast<const double*>(ctx->pin_out.p);
       for (size_t k = 0; k < ok.size(); ++k) {
         t[2 * ok_idx[k]] = o[2 * k];
