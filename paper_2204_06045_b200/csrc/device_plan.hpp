@@ -79,7 +79,7 @@ static_assert(sizeof(DevTensor) == 48, "DevTensor layout");
 //   32..63   tile-number bit (code - 32 = Y bit - cY)
 //   64       stage 1's own summed bit (stage 1 sums at most one var)
 constexpr int kSegYBits = 5;         // cY = min(rY, kSegYBits)
-constexpr int kSegMaxJ = 6;          // digits per segment (dlo/dhi tables: 4 + 2 bits)
+constexpr int kSegMaxJ = 5;          // digits per segment (dlo/dhi tables: 4 + 1 bits)
 constexpr int kSegMaxStages = kSegMaxJ + 1;
 constexpr int kSegMaxOps = 16;       // operands per segment (all stages)
 constexpr int kSegMaxNt1 = 6;        // members of stage 1
