@@ -179,7 +179,8 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
 // Descriptor image of a HostPlan: one contiguous blob, 256-byte aligned sections.
 struct DescLayout {
   size_t ops = 0, ibeg = 0, trefs = 0, segs = 0, seg_ibeg = 0, stages = 0, ctr = 0, scal = 0,
-         lcb = 0, terms = 0, upload = 0, segtab = 0, total = 0;
+         lcb = 0, terms = 0, funits = 0, finit = 0, upload = 0, segtab = 0, fdone = 0, fdeps = 0,
+         fqueue = 0, fstate = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t{255}; }
@@ -197,8 +198,15 @@ DescLayout layout_of(const HostPlan& hp) {
   L.scal = o; o = align256(o + hp.scalar_off.size() * sizeof(uint64_t));
   L.lcb = o; o = align256(o + hp.lc_begin.size() * sizeof(uint32_t));
   L.terms = o; o = align256(o + (hp.lc_begin.size()) * sizeof(double2));
+  L.funits = o; o = align256(o + hp.flow_units.size() * sizeof(FlowUnit));
+  L.finit = o; o = align256(o + hp.flow_init.size() * sizeof(uint64_t));
   L.upload = o;  // device-only sections follow
   L.segtab = o; o = align256(o + (hp.segs.empty() ? 0 : hp.trefs.size() * sizeof(SegOpTab)));
+  const size_t nu = hp.flow_units.size();
+  L.fdone = o; o = align256(o + nu * sizeof(uint32_t));
+  L.fdeps = o; o = align256(o + nu * sizeof(int32_t));
+  L.fqueue = o; o = align256(o + hp.flow_chunks * sizeof(uint64_t));
+  L.fstate = o; o = align256(o + sizeof(FlowState));
   L.total = o;
   return L;
 }
@@ -211,6 +219,8 @@ void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
   std::memcpy(dst + L.seg_ibeg, hp.seg_ibeg.data(), hp.seg_ibeg.size() * sizeof(uint32_t));
   std::memcpy(dst + L.stages, hp.stages.data(), hp.stages.size() * sizeof(DevStage));
   std::memset(dst + L.ctr, 0, hp.levels.size() * 2 * sizeof(uint32_t));  // seg_kernel work counters
+  std::memcpy(dst + L.funits, hp.flow_units.data(), hp.flow_units.size() * sizeof(FlowUnit));
+  std::memcpy(dst + L.finit, hp.flow_init.data(), hp.flow_init.size() * sizeof(uint64_t));
   std::memcpy(dst + L.scal, hp.scalar_off.data(), hp.scalar_off.size() * sizeof(uint64_t));
   std::memcpy(dst + L.lcb, hp.lc_begin.data(), hp.lc_begin.size() * sizeof(uint32_t));
 }
@@ -263,6 +273,8 @@ struct DevProgram {
   const uint32_t* seg_ibeg() const { return reinterpret_cast<const uint32_t*>(base + L.seg_ibeg); }
   const DevStage* stages() const { return reinterpret_cast<const DevStage*>(base + L.stages); }
   SegOpTab* segtab() const { return reinterpret_cast<SegOpTab*>(base + L.segtab); }
+  template <class T>
+  T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
   uint32_t* ctr(size_t level) const { return reinterpret_cast<uint32_t*>(base + L.ctr) + 2 * level; }
   const uint64_t* scal() const { return reinterpret_cast<const uint64_t*>(base + L.scal); }
   const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
@@ -337,7 +349,20 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, vo
                      std::vector<cudaEvent_t>* level_events,
                      std::vector<cudaEvent_t>* kernel_events = nullptr) {
   cudaStream_t s = ctx->stream;
-  for (size_t L = 0; L < hp.levels.size(); ++L) {
+  if (hp.flow) {  // one persistent dataflow kernel instead of the level sequence
+    if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[0], s));
+    const DescLayout& L = pr.L;
+    const auto n = static_cast<uint32_t>(hp.flow_units.size());
+    const auto ni = static_cast<uint32_t>(hp.flow_init.size());
+    QTNG_CUDA((pr.c64 ? c64::launch_flow : c128::launch_flow)(
+        s, pr.at<FlowUnit>(L.funits), n, pr.at<uint64_t>(L.finit), ni,
+        static_cast<uint32_t>(hp.flow_chunks), pr.ops(), pr.segs(), pr.stages(), pr.trefs(),
+        pr.segtab(), arena, pr.at<uint32_t>(L.fdone), pr.at<int32_t>(L.fdeps),
+        pr.at<uint64_t>(L.fqueue), pr.at<FlowState>(L.fstate)));
+    for (size_t k = 1; level_events && k <= hp.levels.size(); ++k)
+      QTNG_CUDA(cudaEventRecord((*level_events)[k], s));
+  }
+  for (size_t L = 0; L < hp.levels.size() && !hp.flow; ++L) {
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
     enqueue_level(ctx, hp.levels[L], L, pr, arena,
                   kernel_events ? kernel_events->data() + 6 * L : nullptr);
@@ -349,6 +374,7 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, vo
 }
 
 int launches_per_run(const HostPlan& hp) {
+  if (hp.flow) return 3;  // flow_reset, flow_kernel, final_kernel
   int lv = 0, outer = 0, seg = 0;
   for (const LevelLaunch& l : hp.levels) {
     lv += l.items > 0;
@@ -793,7 +819,8 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
       QTNG_CUDA(cudaEventElapsedTime(&plan->level_ms[L], plan->lev_ev[L], plan->lev_ev[L + 1]));
     for (float& k : plan->kernel_ms) k = 0.f;
     plan->level_kernel_ms.assign(3 * hp.levels.size(), 0.f);
-    for (size_t L = 0; L < hp.levels.size(); ++L) {
+    if (hp.flow) plan->kernel_ms[2] = plan->level_ms.empty() ? 0.f : plan->level_ms[0];
+    for (size_t L = 0; L < hp.levels.size() && !hp.flow; ++L) {
       const LevelLaunch& lv = hp.levels[L];
       const uint32_t present[3] = {lv.items, lv.outer_items, lv.seg_items};
       for (int k = 0; k < 3; ++k) {

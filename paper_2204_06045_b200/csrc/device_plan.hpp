@@ -150,6 +150,37 @@ struct LevelLaunch {
   uint32_t seg_items;  // tiles
 };
 
+// ---------------------------------------------------------------- dataflow
+// A "flow" program runs every unit (single op or segment) of a plan in ONE
+// persistent kernel: a unit becomes ready when the units producing its
+// materialised inputs have completed (each unit feeds at most one consumer),
+// and warps take work items from the ready units in readiness order -- no
+// level barriers, so small units overlap big ones.
+struct FlowUnit {
+  uint32_t idx;      // into the DevOp array (kind 0) or the DevSeg array (kind 1)
+  uint32_t n_items;  // warp items (ops) or tiles (segments)
+  int32_t succ;      // consuming unit, -1: none (scalar / kept result)
+  uint16_t deps;     // materialised inputs produced by other units
+  uint8_t kind;
+  uint8_t chunk_log;  // items per queue entry = 2^chunk_log
+};
+static_assert(sizeof(FlowUnit) == 16, "FlowUnit layout");
+// queue entry: unit << 32 | chunk index; kFlowEmpty = not yet published
+constexpr uint64_t kFlowEmpty = ~uint64_t{0};
+constexpr uint32_t kFlowMaxChunks = 8192;  // per unit: enough to spread over every warp
+
+// Per-execution state of a flow program (device-only, reset by flow_reset):
+// per unit: items finished and inputs still missing.  Two queues of chunks:
+// "cold" = the chunks ready at start (longest remaining chain first), "hot" =
+// chunks of units that became ready during the run (chain continuations,
+// preferred so the critical path never waits behind bulk work).
+struct FlowState {
+  uint32_t head;   // cold queue (the initially ready chunks): next claim
+  uint32_t tail;   // hot queue (chunks published during the run): publish counter
+  uint32_t hot;    // hot queue: next claim (advanced by CAS, never past `tail`)
+  uint32_t done;   // chunks finished (termination)
+};
+
 // Planner target for warp items per level: enough to cover every SM several
 // times over, so small levels use 1-row items and big levels 32-row items.
 constexpr uint64_t kTargetItems = 16384;

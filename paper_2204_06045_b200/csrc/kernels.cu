@@ -29,6 +29,7 @@
 #include "kernels.cuh"
 
 #include <cstdint>
+#include <cstdio>
 
 #ifndef QTNG_C64
 #define QTNG_C64 0  // 1: the complex64 build of this file (namespace qtng::c64)
@@ -770,6 +771,90 @@ __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
   }
 }
 
+// Per-warp state of the segment currently being evaluated.
+struct SegCursor {
+  int cur = -1;            // segment index whose tables are loaded
+  bool ptab_fresh = false;  // side-product tables built for this segment
+  bool ptab_tile = false;   // ... and they depend on the tile number
+  DevSeg sg{};
+};
+
+// Load segment `si` into the warp state: stages, climb descriptors, per-lane
+// table-index bits.
+__device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const DevSeg* __restrict__ segs,
+                                           int si, const DevStage* __restrict__ stages,
+                                           const SegOpTab* __restrict__ segtab, int lane) {
+  sc.cur = si;
+  sc.sg = segs[si];
+  const DevSeg& sg = sc.sg;
+  __syncwarp();
+  bool tile_dep = false;
+  if (lane < sg.nst) {
+    const DevStage st = stages[sg.stage + lane];
+    cw.st[lane] = st;
+    bool real = lane > 0 && st.nt > 1;  // every side member a real scalar
+    for (int t = 0; real && t < st.nt - 1; ++t)
+      real = __ldg(&segtab[sg.tref + st.op0 + t].kind) == kTensorRealScalar;
+    cw.preal[lane] = real ? 1 : 0;
+    for (int w = 0; w < 2; ++w)
+      tile_dep |= st.ptab && st.u[w] >= kTileSrc && st.u[w] < kSumSrc;
+    const uint32_t mode = st.nt <= 1 ? 0u : (QTNG_SEG_PTAB && st.ptab ? (real ? 2u : 1u) : 3u);
+    uint32_t d = mode;
+    for (int w = 0; w < 2; ++w)
+      if (mode == 1u || mode == 2u) {
+        const uint32_t c = st.u[w];
+        if (c >= kJSrc && c < kTileSrc) d |= ((c - kJSrc) | 32u) << (8 + 8 * w);
+      }
+    cw.sdesc[lane] = d;
+  }
+  __syncwarp();
+  for (int i = 0; i < sg.nst; ++i) {  // lane bits of each table index
+    const DevStage st = cw.st[i];
+    uint32_t b = 0;
+    for (int w = 0; w < 2; ++w)
+      if (st.u[w] < kLaneSrcEnd) b |= ((static_cast<uint32_t>(lane) >> st.u[w]) & 1u) << (1 + w);
+    cw.slane[i][lane] = static_cast<uint8_t>(b);
+  }
+  // the side-product tables depend on the tile only through tile-bit u's
+  sc.ptab_tile = __any_sync(kFull, tile_dep);
+  sc.ptab_fresh = false;
+}
+
+// One tile of the loaded segment.
+__device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t tile,
+                                         const DevTensor* __restrict__ trefs,
+                                         const SegOpTab* __restrict__ segtab,
+                                         V* __restrict__ arena, int lane) {
+  const DevSeg& sg = sc.sg;
+  const SegOpTab* tab = segtab + sg.tref;
+  for (int op = 0; op < sg.nops; ++op) {
+    const uint32_t v = ((tile >> lane) & 1u) ? __ldg(&tab[op].dtile[lane]) : 0u;
+    const uint32_t sum = __reduce_add_sync(kFull, v);
+    if (lane == 0) cw.toff[op] = sum;
+  }
+  if (!sc.ptab_fresh || sc.ptab_tile) {
+    chain_ptab_build(cw, sg, trefs, arena, tile, lane);
+    sc.ptab_fresh = true;
+  }
+  __syncwarp();
+  const DevStage s1 = cw.st[0];
+  switch (s1.nt * 2 + s1.ns) {
+    case 2: chain_tile_u<1, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 3: chain_tile_u<1, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 4: chain_tile_u<2, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 5: chain_tile_u<2, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 6: chain_tile_u<3, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 7: chain_tile_u<3, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 8: chain_tile_u<4, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 9: chain_tile_u<4, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 10: chain_tile_u<5, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 11: chain_tile_u<5, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 12: chain_tile_u<6, 0>(cw, tab, sg, arena, tile, lane); break;
+    default: chain_tile_u<6, 1>(cw, tab, sg, arena, tile, lane); break;
+  }
+  __syncwarp();
+}
+
 #ifndef QTNG_SEG_MINB
 #define QTNG_SEG_MINB 32  // resident one-warp CTAs per SM (tuned: 32 = the per-SM block limit)
 #endif
@@ -782,94 +867,138 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
   const int lane = threadIdx.x;
   // dynamic tile queue (segments are sorted by per-tile cost, largest first);
   // ctr[0] = next tile, ctr[1] = finished warps; the last warp resets both
-  int cur = -1;
+  SegCursor sc;
   uint32_t cur_begin = 0, cur_end = 0;
-  bool ptab_fresh = false, ptab_tile = false;
-  DevSeg sg{};
   uint32_t nxt = 0;  // the next tile is fetched while the current one runs
   if (lane == 0) nxt = atomicAdd(ctr, 1u);
   for (;;) {
     const uint32_t item = __shfl_sync(kFull, nxt, 0);
     if (item >= items) break;
     if (lane == 0) nxt = atomicAdd(ctr, 1u);
-    if (cur < 0 || item < cur_begin || item >= cur_end) {
+    if (sc.cur < 0 || item < cur_begin || item >= cur_end) {
       uint32_t lo = 0, hi = seg_count;
       while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
         if (__ldg(ibeg + mid) <= item) lo = mid; else hi = mid;
       }
-      if (static_cast<int>(lo) != cur) {
-        cur = static_cast<int>(lo);
-        sg = segs[lo];
-        __syncwarp();
-        bool tile_dep = false;
-        if (lane < sg.nst) {
-          const DevStage st = stages[sg.stage + lane];
-          cw.st[lane] = st;
-          bool real = lane > 0 && st.nt > 1;  // every side member a real scalar
-          for (int t = 0; real && t < st.nt - 1; ++t)
-            real = __ldg(&segtab[sg.tref + st.op0 + t].kind) == kTensorRealScalar;
-          cw.preal[lane] = real ? 1 : 0;
-          for (int w = 0; w < 2; ++w)
-            tile_dep |= st.ptab && st.u[w] >= kTileSrc && st.u[w] < kSumSrc;
-          const uint32_t mode = st.nt <= 1 ? 0u : (QTNG_SEG_PTAB && st.ptab ? (real ? 2u : 1u) : 3u);
-          uint32_t d = mode;
-          for (int w = 0; w < 2; ++w)
-            if (mode == 1u || mode == 2u) {
-              const uint32_t c = st.u[w];
-              if (c >= kJSrc && c < kTileSrc) d |= ((c - kJSrc) | 32u) << (8 + 8 * w);
-            }
-          cw.sdesc[lane] = d;
-        }
-        __syncwarp();
-        for (int i = 0; i < sg.nst; ++i) {  // lane bits of each table index
-          const DevStage st = cw.st[i];
-          uint32_t b = 0;
-          for (int w = 0; w < 2; ++w)
-            if (st.u[w] < kLaneSrcEnd) b |= ((static_cast<uint32_t>(lane) >> st.u[w]) & 1u) << (1 + w);
-          cw.slane[i][lane] = static_cast<uint8_t>(b);
-        }
-        // the side-product tables depend on the tile only through tile-bit u's
-        ptab_tile = __any_sync(kFull, tile_dep);
-        ptab_fresh = false;
-      }
+      if (static_cast<int>(lo) != sc.cur) seg_switch(cw, sc, segs, static_cast<int>(lo), stages, segtab, lane);
       cur_begin = __ldg(ibeg + lo);
       cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
     }
-    const uint32_t tile = item - cur_begin;
-    const SegOpTab* tab = segtab + sg.tref;
-    for (int op = 0; op < sg.nops; ++op) {
-      const uint32_t v = ((tile >> lane) & 1u) ? __ldg(&tab[op].dtile[lane]) : 0u;
-      const uint32_t sum = __reduce_add_sync(kFull, v);
-      if (lane == 0) cw.toff[op] = sum;
-    }
-    if (!ptab_fresh || ptab_tile) {
-      chain_ptab_build(cw, sg, trefs, arena, tile, lane);
-      ptab_fresh = true;
-    }
-    __syncwarp();
-    const DevStage s1 = cw.st[0];
-    switch (s1.nt * 2 + s1.ns) {
-      case 2: chain_tile_u<1, 0>(cw, tab, sg, arena, tile, lane); break;
-      case 3: chain_tile_u<1, 1>(cw, tab, sg, arena, tile, lane); break;
-      case 4: chain_tile_u<2, 0>(cw, tab, sg, arena, tile, lane); break;
-      case 5: chain_tile_u<2, 1>(cw, tab, sg, arena, tile, lane); break;
-      case 6: chain_tile_u<3, 0>(cw, tab, sg, arena, tile, lane); break;
-      case 7: chain_tile_u<3, 1>(cw, tab, sg, arena, tile, lane); break;
-      case 8: chain_tile_u<4, 0>(cw, tab, sg, arena, tile, lane); break;
-      case 9: chain_tile_u<4, 1>(cw, tab, sg, arena, tile, lane); break;
-      case 10: chain_tile_u<5, 0>(cw, tab, sg, arena, tile, lane); break;
-      case 11: chain_tile_u<5, 1>(cw, tab, sg, arena, tile, lane); break;
-      case 12: chain_tile_u<6, 0>(cw, tab, sg, arena, tile, lane); break;
-      default: chain_tile_u<6, 1>(cw, tab, sg, arena, tile, lane); break;
-    }
-    __syncwarp();
+    seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane);
   }
   if (lane == 0) {
     __threadfence();
     if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every warp has left the queue
       ctr[0] = 0;
       ctr[1] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- dataflow
+// flow_reset: the per-execution state of a flow program.
+__global__ void flow_reset(const FlowUnit* __restrict__ units, uint32_t n_units,
+                           const uint64_t* __restrict__ init, uint32_t n_init, uint32_t n_chunks,
+                           uint32_t* __restrict__ done, int32_t* __restrict__ deps,
+                           uint64_t* __restrict__ queue, FlowState* __restrict__ st) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_units) {
+    done[i] = 0;
+    deps[i] = units[i].deps;
+  }
+  if (i < n_chunks) queue[i] = i < n_init ? init[i] : kFlowEmpty;  // hot queue: [n_init, n_chunks)
+  if (i == 0) {
+    st->head = 0;
+    st->tail = n_init;
+    st->hot = n_init;
+    st->done = 0;
+  }
+}
+
+// Run one work item of a single-op unit (the level kernel's item code).
+__device__ __forceinline__ void flow_op_item(const DevOp& op, uint32_t item,
+                                             const DevTensor* __restrict__ trefs, V* __restrict__ arena,
+                                             int lane, DevTensor* slot) {
+  switch (op.nt) {
+    case 1: dispatch_ns<1>(op, item, trefs, arena, lane, slot); break;
+    case 2: dispatch_ns<2>(op, item, trefs, arena, lane, slot); break;
+    case 3: dispatch_ns<3>(op, item, trefs, arena, lane, slot); break;
+    case 4: dispatch_ns<4>(op, item, trefs, arena, lane, slot); break;
+    case 5: dispatch_ns<5>(op, item, trefs, arena, lane, slot); break;
+    case 6: dispatch_ns<6>(op, item, trefs, arena, lane, slot); break;
+    case 7: dispatch_ns<7>(op, item, trefs, arena, lane, slot); break;
+    default: dispatch_ns<8>(op, item, trefs, arena, lane, slot); break;
+  }
+}
+
+// flow_kernel: a persistent warp claims the next queue position (one atomic),
+// waits until that position is published, runs the chunk's items with the
+// level-kernel or segment-kernel code, and counts them done; the warp that
+// finishes a unit decrements its consumer's missing inputs and, at zero,
+// appends all of the consumer's chunks to the queue.  Producers fence before
+// counting, consumers fence after reading a published entry; outputs never
+// share an arena region (no L1 line can be stale).
+__global__ void __launch_bounds__(32, QTNG_SEG_MINB)
+flow_kernel(const FlowUnit* __restrict__ units, uint32_t n_init, uint32_t n_chunks,
+            const DevOp* __restrict__ ops,
+            const DevSeg* __restrict__ segs, const DevStage* __restrict__ stages,
+            const DevTensor* __restrict__ trefs, const SegOpTab* __restrict__ segtab,
+            V* __restrict__ arena, uint32_t* __restrict__ done, int32_t* __restrict__ deps,
+            volatile uint64_t* queue, FlowState* st) {
+  __shared__ ChainWarp cw;
+  __shared__ DevTensor slot[kMaxInputs];
+  const int lane = threadIdx.x;
+  SegCursor sc;
+  for (;;) {
+    uint64_t e = kFlowEmpty;
+    bool quit = false;
+    if (lane == 0) {
+      // hot first (chain continuations) when some are published; else cold;
+      // with cold exhausted, claim a hot position and wait for it -- every hot
+      // position [n_init, n_chunks) is published exactly once
+      const uint32_t h = *reinterpret_cast<volatile uint32_t*>(&st->hot);
+      const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&st->tail);
+      uint32_t c = n_init;
+      if (!(h < t) && *reinterpret_cast<volatile uint32_t*>(&st->head) < n_init)
+        c = atomicAdd(&st->head, 1u);
+      if (c < n_init) {
+        e = queue[c];
+      } else {
+        const uint32_t p = atomicAdd(&st->hot, 1u);
+        if (p >= n_chunks) {
+          quit = true;
+        } else {
+          while ((e = queue[p]) == kFlowEmpty) __nanosleep(128);
+        }
+      }
+      __threadfence();  // acquire: the producers' results are visible
+    }
+    if (__shfl_sync(kFull, quit ? 1 : 0, 0)) break;
+    e = __shfl_sync(kFull, e, 0);
+    const uint32_t u = static_cast<uint32_t>(e >> 32), c = static_cast<uint32_t>(e);
+    const FlowUnit f = units[u];
+    const uint32_t i0 = c << f.chunk_log, i1 = min(f.n_items, (c + 1) << f.chunk_log);
+    if (f.kind) {
+      if (sc.cur != static_cast<int>(f.idx)) seg_switch(cw, sc, segs, static_cast<int>(f.idx), stages, segtab, lane);
+      for (uint32_t item = i0; item < i1; ++item) seg_tile(cw, sc, item, trefs, segtab, arena, lane);
+    } else {
+      const DevOp op = ops[f.idx];
+      for (uint32_t item = i0; item < i1; ++item) flow_op_item(op, item, trefs, arena, lane, slot);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();  // this chunk's results before its count
+      if (atomicAdd(done + u, i1 - i0) + (i1 - i0) == f.n_items && f.succ >= 0) {
+        __threadfence();
+        if (atomicSub(deps + f.succ, 1) == 1) {  // the consumer is ready: publish its chunks
+          const FlowUnit g = units[f.succ];
+          const uint32_t nc = (g.n_items + (1u << g.chunk_log) - 1) >> g.chunk_log;
+          const uint32_t base = atomicAdd(&st->tail, nc);
+          for (uint32_t k = 0; k < nc; ++k)
+            queue[base + k] = (static_cast<uint64_t>(f.succ) << 32) | k;
+        }
+      }
     }
   }
 }
@@ -946,6 +1075,28 @@ cudaError_t launch_outer(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
   outer_kernel<<<outer_grid(lv.outer_items), kThreads, 0, s>>>(ops + first, ibeg + first, trefs,
                                                                arena, lv.outer_count,
                                                                lv.outer_items);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flow(cudaStream_t s, const FlowUnit* units, uint32_t n_units,
+                        const uint64_t* init, uint32_t n_init, uint32_t n_chunks, const DevOp* ops,
+                        const DevSeg* segs, const DevStage* stages, const DevTensor* trefs,
+                        const SegOpTab* segtab, void* arena_v, uint32_t* done, int32_t* deps,
+                        uint64_t* queue, FlowState* st) {
+  if (n_units == 0) return cudaSuccess;
+  const uint32_t n = n_units > n_chunks ? n_units : n_chunks;
+  flow_reset<<<(n + 255) / 256, 256, 0, s>>>(units, n_units, init, n_init, n_chunks, done, deps,
+                                             queue, st);
+  static int cap = 0;
+  if (cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, 32, 0);
+    cap = sms * (per_sm > 0 ? per_sm : 1);  // persistent: every CTA resident
+  }
+  flow_kernel<<<cap, 32, 0, s>>>(units, n_init, n_chunks, ops, segs, stages, trefs, segtab,
+                                 static_cast<V*>(arena_v), done, deps, queue, st);
   return cudaGetLastError();
 }
 

@@ -33,6 +33,12 @@ namespace qtng {
   /* the segments' SegOpTab entries (once per descriptor upload) */                           \
   cudaError_t launch_seg_prep(cudaStream_t s, const DevSeg* segs, uint32_t n_segs,             \
                               const DevTensor* trefs, SegOpTab* segtab);                       \
+  /* a whole dataflow program in one persistent kernel (after its state reset) */             \
+  cudaError_t launch_flow(cudaStream_t s, const FlowUnit* units, uint32_t n_units,             \
+                          const uint64_t* init, uint32_t n_init, uint32_t n_chunks,           \
+                          const DevOp* ops, const DevSeg* segs, const DevStage* stages,       \
+                          const DevTensor* trefs, const SegOpTab* segtab, void* arena,        \
+                          uint32_t* done, int32_t* deps, uint64_t* queue, FlowState* st);      \
   /* resident warps of the level kernel on the current device */                              \
   int resident_warps();                                                                        \
   /* per lightcone: e_jk = prod of its scalar results in production order (complex128) */     \

@@ -80,6 +80,14 @@ int seg_max_j() {
   return j;
 }
 
+bool flow_default() {
+  static const bool on = [] {
+    const char* v = std::getenv("QTNG_FLOW");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 bool fuse_default() {
   static const bool on = [] {
     const char* v = std::getenv("QTNG_FUSE");
@@ -89,7 +97,7 @@ bool fuse_default() {
 }
 
 HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems, bool fuse,
-                    bool qaoa_gates) {
+                    bool qaoa_gates, bool flow) {
   HostPlan hp;
   hp.input_elems = input_elems;
   const int C = static_cast<int>(cones.size());
@@ -236,7 +244,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   ClassArena arena(round_up(input_elems, kAlign));
   auto cls_of = [&](uint32_t u) { return std::max<int>(op_at(unit_last[u]).r, kMinClass); };
   for (int L = 0; L < n_levels; ++L) {
-    if (L > 0)
+    if (L > 0 && !flow)  // flow programs never reuse a region
       for (uint32_t i = rstart[L - 1]; i < rstart[L]; ++i)
         arena.release(cls_of(rel[i]), out[unit_last[rel[i]]]);
     for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i)
@@ -513,6 +521,55 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
         ++hp.n_buckets;
         hp.max_width = std::max(hp.max_width, static_cast<int>(o.width));
       }
+    }
+  }
+
+  if (flow) {
+    hp.flow = true;
+    hp.flow_units.resize(U);
+    std::vector<int32_t> height(U, 0);  // units on the longest path to a sink
+    for (int64_t i = static_cast<int64_t>(U) - 1; i >= 0; --i) {  // descending level
+      const uint32_t u = order[static_cast<size_t>(i)];
+      const int64_t cu = consumer_unit(u);
+      height[u] = cu >= 0 ? height[cu] + 1 : 0;
+    }
+    for (uint32_t u = 0; u < U; ++u) {
+      FlowUnit& f = hp.flow_units[u];
+      f = FlowUnit{};
+      f.kind = unit_len[u] > 1 ? 1 : 0;
+      f.idx = unit_slot[u];
+      if (f.kind) {
+        const DevSeg& sg = hp.segs[f.idx];
+        f.n_items = 1u << (sg.ry - sg.cy);
+      } else {
+        const DevOp& d = hp.ops[f.idx];
+        f.n_items = 1u << (d.r - d.cb);
+      }
+      f.succ = static_cast<int32_t>(consumer_unit(u));
+      const uint32_t c = lc_of[unit_first[u]];
+      const WalkResult& w = *cones[c];
+      int deps = 0;
+      for (uint32_t g = unit_first[u]; g != ~0u; g = next_in_unit[g]) {
+        const Op& o = op_at(g);
+        const OpIn* ins = w.inputs(o);
+        for (int t = 0; t < o.nin; ++t)
+          if (!ins[t].initial && t != main_pos[g]) ++deps;
+      }
+      f.deps = static_cast<uint16_t>(deps);
+      int cl = 0;
+      while ((f.n_items >> cl) > kFlowMaxChunks) ++cl;
+      f.chunk_log = static_cast<uint8_t>(cl);
+      hp.flow_chunks += (f.n_items + (1u << cl) - 1) >> cl;
+    }
+    std::vector<uint32_t> init;
+    for (uint32_t u = 0; u < U; ++u)
+      if (hp.flow_units[u].deps == 0) init.push_back(u);
+    std::stable_sort(init.begin(), init.end(),
+                     [&](uint32_t a, uint32_t b) { return height[a] > height[b]; });
+    for (uint32_t u : init) {
+      const FlowUnit& f = hp.flow_units[u];
+      const uint32_t nc = (f.n_items + (1u << f.chunk_log) - 1) >> f.chunk_log;
+      for (uint32_t c = 0; c < nc; ++c) hp.flow_init.push_back((uint64_t{u} << 32) | c);
     }
   }
 

@@ -26,6 +26,11 @@ struct HostPlan {
   double dev_bytes = 0;
   uint64_t n_fused_ops = 0;            // ops evaluated inside segments
   bool c64 = false;                    // complex64 arena/kernels (set by the caller)
+  // dataflow program (flow=true): every unit in one persistent kernel
+  bool flow = false;
+  std::vector<FlowUnit> flow_units;    // indexed by unit id
+  std::vector<uint64_t> flow_init;     // queue entries ready at start (longest remaining chain first)
+  uint64_t flow_chunks = 0;            // total queue entries of one execution
   double fp64_ops = 0;                 // the reference's FP64 mul/add count (all ops)
   double seg_fp64_ops = 0;             // ... of the ops inside segments
   double single_alg_bytes = 0;         // B_alg of the single (level/outer kernel) ops
@@ -49,6 +54,8 @@ struct HostPlan {
 
 // Default for build_plan's `fuse`: on unless QTNG_FUSE=0.
 bool fuse_default();
+// Default for build_plan's `flow`: QTNG_FLOW=1.
+bool flow_default();
 
 // Plans `cones` (each the walk of one lightcone's schedule) onto one arena
 // whose first `input_elems` elements hold the inputs.  Chains of buckets whose
@@ -56,7 +63,10 @@ bool fuse_default();
 // fuse=false keeps every op a separate level-kernel op (no chain fusion).
 // qaoa_gates: the input region is the QAOA gate table (fill_gate_table), so
 // initial operands are classified by gate slot (DevTensor::kind).
+// flow: build a dataflow program (no arena reuse: every unit's output gets its
+// own region, so no warp can hold a stale L1 line of it).
 HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems,
-                    bool fuse = fuse_default(), bool qaoa_gates = false);
+                    bool fuse = fuse_default(), bool qaoa_gates = false,
+                    bool flow = flow_default());
 
 }  // namespace qtng

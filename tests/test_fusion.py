@@ -103,3 +103,12 @@ def test_fused_equals_unfused_bitwise(golden, name):
         assert fused["terms"] == plain["terms"], f"QTNG_SEG_J={j}"
     got = np.array([complex(x, y) for x, y in plain["terms"]])
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+def test_flow_executor_bitwise(golden):
+    # the experimental single-kernel dataflow executor (QTNG_FLOW=1) runs the
+    # same units: terms identical to the level-synchronous program's
+    ref = [[x, y] for x, y in golden["configs"]["C2"]["terms_naive"]]
+    flow = _child_energy("C2", {"QTNG_FLOW": "1"})
+    assert flow["terms"] == ref
