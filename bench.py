@@ -296,6 +296,9 @@ def run_b200(args, cfg):
 
     # largest-bucket level in isolation (C3-class microbench on real buckets)
     big_level, big_bytes, big_ms = plan.time_level(-1, 20)
+    # BASELINE configs[2]: the calibration bucket [w,2]->w-1 (engine.cpp:371-390)
+    # as one level_kernel op, HBM-bound, timed alone (rank 0 only)
+    c3 = microbench_c3(ctx) if rank == 0 and not args.no_c3 else None
 
     if rank != 0:
         return 0
@@ -365,6 +368,7 @@ def run_b200(args, cfg):
                                   "(SURVEY 8a); dev_bytes = what the fused program must move"},
         "roofline_largest_level": {"level": big_level, "alg_bytes": big_bytes, "ms": big_ms,
                                    "effective_GBps": big_bytes / (big_ms / 1e3) / 1e9},
+        "microbench_c3": c3,
         "clocks": csum,
         "gpu_launches": int(args.steps * (info.kernels_per_run * 3 + (1 if info.n_segments else 0))),
         "arena_bytes": int(info.arena_bytes),
@@ -376,6 +380,31 @@ def run_b200(args, cfg):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def microbench_c3(ctx, widths=(26, 28)):
+    """The single-bucket microbench (BASELINE configs[2]): calibrate()'s
+    synthetic bucket, a rank-w tensor times a rank-2 one summing the MSB var
+    ([w, 2] -> w-1, 16*(2^w + 4 + 2^(w-1)) algorithmic bytes), contracted by
+    level_kernel alone; CUDA events around 10 back-to-back launches."""
+    import numpy as np
+    import paper_2204_06045_b200 as q
+    peak, kind = load_peaks()
+    rng = np.random.default_rng(7)
+    out = {"peak_GBps": peak, "peak_source": kind, "cases": []}
+    for w in widths:
+        a = rng.uniform(-1, 1, 1 << w) + 1j * rng.uniform(-1, 1, 1 << w)
+        b = rng.uniform(-1, 1, 4) + 1j * rng.uniform(-1, 1, 4)
+        sch = q.ContractionSchedule([q.Bucket([0], [q.Tensor("a", list(range(w)), a),
+                                                    q.Tensor("b", [0, 1], b)])])
+        plan = q.Plan.from_schedule(sch, ctx=ctx)
+        plan.execute()
+        _, by, ms = plan.time_level(0, 10)
+        plan.close()
+        gbs = by / (ms * 1e-3) / 1e9
+        out["cases"].append({"bucket": f"[{w},2]->{w - 1}", "alg_bytes": by, "ms": ms,
+                             "GBps": gbs, "frac": gbs / peak})
+    return out
 
 
 def cpu_baseline(cfg):
@@ -411,6 +440,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the single-bucket microbench")
     ap.add_argument("--dtype", choices=["c128", "c64"], default="c128",
                     help="c64: the optional complex64 mode (1e-5), not the headline")
     args = ap.parse_args()

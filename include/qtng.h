@@ -127,6 +127,12 @@ qtng_status qtng_simulate_widths(int n, int m, const int* edges, int p, int edge
 qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged,
                             double* bytes_out);
 
+/* Predicted device work per edge lightcone (the sharding key of the
+ * multi-GPU driver): per bucket 2^width * max(1, members-1) complex products
+ * plus the summation adds -- the fused program is bound by arithmetic and
+ * issue, not by bytes.  m doubles. */
+qtng_status qtng_edge_work(int n, int m, const int* edges, int p, int merged, double* work_out);
+
 /* Host-only pre-flight of energy_expectation: builds every edge's schedule and
  * runs the data-free contract_network walk (liveness / result-width cap /
  * routing checks, engine.cpp:160-169,246-304) and reports the first refusal

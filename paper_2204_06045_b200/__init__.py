@@ -431,6 +431,14 @@ def edge_costs(g: Graph, p: int, merged: bool = False) -> np.ndarray:
     return out[: g.m]
 
 
+def edge_work(g: Graph, p: int, merged: bool = False) -> np.ndarray:
+    """Predicted device work per edge lightcone (complex products + adds of
+    the reference loop): the multi-GPU sharding key."""
+    out = np.zeros(max(1, g.m), dtype=np.float64)
+    _check(lib.qtng_edge_work(g.n, g.m, g.flat(), p, int(merged), out))
+    return out[: g.m]
+
+
 def plan_dump(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfig] = None,
               edges: Optional[Sequence[int]] = None) -> List[dict]:
     """Host-only description of the device program (one dict per device op,

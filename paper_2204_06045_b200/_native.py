@@ -60,6 +60,7 @@ def _load():
     lib.qtng_simulate_widths.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int,
                                          i32p, C.c_int, C.POINTER(C.c_int)]
     lib.qtng_edge_costs.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, f64p]
+    lib.qtng_edge_work.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, f64p]
     lib.qtng_validate_energy.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int]
     lib.qtng_plan_dump.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_void_p, i32p, C.c_int64, C.POINTER(C.c_int64),
@@ -100,7 +101,7 @@ lib = _load()
 # Every symbol include/qtng.h declares (checked by tests/test_abi.py).
 EXPORTED = [
     "qtng_create", "qtng_destroy", "qtng_last_error", "qtng_version", "qtng_random_regular",
-    "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
+    "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_edge_work", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
     "qtng_contract_schedule", "qtng_energy", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute",
     "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_set_precision", "qtng_statevector_energy", "qtng_plan_segments", "qtng_plan_records", "qtng_plan_level_ms", "qtng_plan_kernel_ms",
     "qtng_plan_destroy", "qtng_plan_time_level",

@@ -543,6 +543,20 @@ qtng_status qtng_edge_costs(int n, int m, const int* edges, int p, int merged, d
   });
 }
 
+qtng_status qtng_edge_work(int n, int m, const int* edges, int p, int merged, double* work_out) {
+  return guarded([&] {
+    const Graph g = graph_from(n, m, edges);
+    const ConeSet cs = plan_cones(g, p, merged != 0, 1 << 20, selection(m, m, nullptr));
+    for (int i = 0; i < m; ++i) {
+      double fl = 0;  // the reference loop's complex products + additions per lightcone
+      for (const Op& op : cs.walks[i].ops)
+        fl += std::ldexp(1.0, op.width) * std::max(1, op.nin - 1) +
+              std::ldexp(1.0, op.r) * (std::ldexp(1.0, op.ns) - 1.0);
+      work_out[i] = fl;
+    }
+  });
+}
+
 qtng_status qtng_validate_energy(int n, int m, const int* edges, int p, int merged,
                                  int max_result_width) {
   return guarded([&] {

@@ -838,6 +838,10 @@ __device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t 
   }
   __syncwarp();
   const DevStage s1 = cw.st[0];
+#ifdef QTNG_SASS_ONE_SHAPE  // SASS inspection build: only the dominant head shape
+  chain_tile_u<3, 1>(cw, tab, sg, arena, tile, lane);
+  return;
+#endif
   switch (s1.nt * 2 + s1.ns) {
     case 2: chain_tile_u<1, 0>(cw, tab, sg, arena, tile, lane); break;
     case 3: chain_tile_u<1, 1>(cw, tab, sg, arena, tile, lane); break;

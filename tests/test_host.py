@@ -138,3 +138,15 @@ def test_merged_schedule_keeps_widths_bounded(q):
         wm = q.simulate_widths(g, i, 2, merged=True)
         assert max(wm) <= max(wu)
         assert len(wm) <= len(wu)
+
+
+def test_edge_work_is_the_reference_op_count(q, golden):
+    # per lightcone: sum over buckets of 2^width * max(1, members-1) + adds;
+    # summed over C2 it bounds the reference's ops (sum 2^width) from above
+    c = golden["configs"]["C2"]
+    g = q.random_regular(c["n"], 3, c["seed"])
+    w = q.edge_work(g, 4)
+    assert w.shape == (g.m,) and (w > 0).all()
+    ops = q.plan_stats(g, 4).sum_ops
+    assert w.sum() >= ops
+    assert w.argmax() == q.edge_costs(g, 4).argmax()

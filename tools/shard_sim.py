@@ -12,7 +12,7 @@ from paper_2204_06045_b200 import dist  # noqa: E402
 
 g, a = q.random_regular(30, 3, 104478), q.Angles([0.30, 0.25, 0.20, 0.15], [0.35, 0.30, 0.25, 0.20])
 ctx = q.Context(0)
-costs = q.edge_costs(g, 4)
+costs = q.edge_work(g, 4) if os.environ.get('SHARD_KEY', 'work') == 'work' else q.edge_costs(g, 4)
 for n in (1, 2, 4, 8):
     times = []
     for shard in dist.lpt_shard(costs, n):
