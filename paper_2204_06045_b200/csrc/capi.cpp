@@ -229,6 +229,17 @@ void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
 
 // ---------------------------------------------------------------- context
 
+// An independent stream set + buffers: the one-shot energy pipelines two
+// halves of the lightcones through two lanes (host planning of the second
+// half overlaps the device work of the first).
+struct Lane {
+  cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
+  cudaEvent_t fork = nullptr, join2 = nullptr, join3 = nullptr;
+  DevBuf* arena = nullptr;
+  DevBuf* desc = nullptr;
+  PinBuf *pin_desc = nullptr, *pin_in = nullptr, *pin_out = nullptr;
+};
+
 struct qtng_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -242,6 +253,9 @@ struct qtng_ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, join3_ev = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf sv_scratch;     // state-vector oracle: edge bits, per-edge sums, partials
+  Lane lane[2];          // lane 0 aliases the fields above; lane 1 owns its own
+  DevBuf arena1, desc1;
+  PinBuf pin_desc1, pin_in1, pin_out1;
   int prec = 128;        // QAOA plans / energies: 128 = complex128, 64 = complex64
 
   // arena of `elems` elements of `elem_bytes` (16: double2, 8: float2)
@@ -286,37 +300,38 @@ struct DevProgram {
 // kev (optional): 6 events bracketing this level's level / outer / segment
 // kernels on the streams they run on (per-kernel device time).
 void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const DevProgram& pr,
-                   void* arena, cudaEvent_t* kev = nullptr) {
+                   void* arena, cudaEvent_t* kev = nullptr, const Lane* ln = nullptr) {
+  const Lane& la = ln ? *ln : ctx->lane[0];
   const bool c64 = pr.c64;
   const bool fork2 = lv.outer_items > 0;
   const bool fork3 = lv.seg_items > 0 && (lv.items > 0 || fork2);
   auto rec = [&](int k, cudaStream_t st) {
     if (kev) QTNG_CUDA(cudaEventRecord(kev[k], st));
   };
-  if (fork2 || fork3) QTNG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+  if (fork2 || fork3) QTNG_CUDA(cudaEventRecord(la.fork, la.s));
   if (fork2) {
-    QTNG_CUDA(cudaStreamWaitEvent(ctx->stream2, ctx->fork_ev, 0));
-    rec(2, ctx->stream2);
-    QTNG_CUDA(c64 ? c64::launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv)
-                  : c128::launch_outer(ctx->stream2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
-    rec(3, ctx->stream2);
-    QTNG_CUDA(cudaEventRecord(ctx->join_ev, ctx->stream2));
+    QTNG_CUDA(cudaStreamWaitEvent(la.s2, la.fork, 0));
+    rec(2, la.s2);
+    QTNG_CUDA(c64 ? c64::launch_outer(la.s2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv)
+                  : c128::launch_outer(la.s2, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+    rec(3, la.s2);
+    QTNG_CUDA(cudaEventRecord(la.join2, la.s2));
   }
-  cudaStream_t s3 = fork3 ? ctx->stream3 : ctx->stream;
-  if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream3, ctx->fork_ev, 0));
+  cudaStream_t s3 = fork3 ? la.s3 : la.s;
+  if (fork3) QTNG_CUDA(cudaStreamWaitEvent(la.s3, la.fork, 0));
   rec(4, s3);
   QTNG_CUDA(c64 ? c64::launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
                                     pr.segtab(), arena, pr.ctr(level), lv)
                 : c128::launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
                                     pr.segtab(), arena, pr.ctr(level), lv));
   rec(5, s3);
-  if (fork3) QTNG_CUDA(cudaEventRecord(ctx->join3_ev, ctx->stream3));
-  rec(0, ctx->stream);
-  QTNG_CUDA(c64 ? c64::launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv)
-                : c128::launch_level(ctx->stream, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
-  rec(1, ctx->stream);
-  if (fork2) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
-  if (fork3) QTNG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join3_ev, 0));
+  if (fork3) QTNG_CUDA(cudaEventRecord(la.join3, la.s3));
+  rec(0, la.s);
+  QTNG_CUDA(c64 ? c64::launch_level(la.s, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv)
+                : c128::launch_level(la.s, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));
+  rec(1, la.s);
+  if (fork2) QTNG_CUDA(cudaStreamWaitEvent(la.s, la.join2, 0));
+  if (fork3) QTNG_CUDA(cudaStreamWaitEvent(la.s, la.join3, 0));
 }
 
 size_t elem_bytes(const HostPlan& hp) { return hp.c64 ? sizeof(float2) : sizeof(double2); }
@@ -334,12 +349,14 @@ void stage_input(const HostPlan& hp, const double* in, uint64_t elems, void* dst
 
 // Upload a HostPlan's descriptor image to `dev` (layout L) on the context
 // stream and build its device-only segment tables.
-void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* dev) {
-  ctx->pin_desc.ensure(L.upload);
-  pack_desc(hp, L, static_cast<char*>(ctx->pin_desc.p));
-  QTNG_CUDA(cudaMemcpyAsync(dev, ctx->pin_desc.p, L.upload, cudaMemcpyHostToDevice, ctx->stream));
+void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* dev,
+                 const Lane* ln = nullptr) {
+  const Lane& la = ln ? *ln : ctx->lane[0];
+  la.pin_desc->ensure(L.upload);
+  pack_desc(hp, L, static_cast<char*>(la.pin_desc->p));
+  QTNG_CUDA(cudaMemcpyAsync(dev, la.pin_desc->p, L.upload, cudaMemcpyHostToDevice, la.s));
   const DevProgram pr{dev, L, hp.c64};
-  QTNG_CUDA(c128::launch_seg_prep(ctx->stream, pr.segs(), static_cast<uint32_t>(hp.segs.size()), pr.trefs(),
+  QTNG_CUDA(c128::launch_seg_prep(la.s, pr.segs(), static_cast<uint32_t>(hp.segs.size()), pr.trefs(),
                             pr.segtab()));
 }
 
@@ -347,8 +364,9 @@ void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* d
 // per-lightcone products.
 void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, void* arena,
                      std::vector<cudaEvent_t>* level_events,
-                     std::vector<cudaEvent_t>* kernel_events = nullptr) {
-  cudaStream_t s = ctx->stream;
+                     std::vector<cudaEvent_t>* kernel_events = nullptr, const Lane* ln = nullptr) {
+  const Lane& la = ln ? *ln : ctx->lane[0];
+  cudaStream_t s = la.s;
   if (hp.flow) {  // one persistent dataflow kernel instead of the level sequence
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[0], s));
     const DescLayout& L = pr.L;
@@ -365,7 +383,7 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, vo
   for (size_t L = 0; L < hp.levels.size() && !hp.flow; ++L) {
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
     enqueue_level(ctx, hp.levels[L], L, pr, arena,
-                  kernel_events ? kernel_events->data() + 6 * L : nullptr);
+                  kernel_events ? kernel_events->data() + 6 * L : nullptr, &la);
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
   QTNG_CUDA((pr.c64 ? c64::launch_final : c128::launch_final)(
@@ -445,6 +463,19 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
     QTNG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
     QTNG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     QTNG_CUDA(cudaEventCreateWithFlags(&ctx->join3_ev, cudaEventDisableTiming));
+    Lane& l0 = ctx->lane[0];
+    l0 = Lane{ctx->stream, ctx->stream2, ctx->stream3, ctx->fork_ev, ctx->join_ev, ctx->join3_ev,
+              &ctx->arena, &ctx->desc, &ctx->pin_desc, &ctx->pin_in, &ctx->pin_out};
+    Lane& l1 = ctx->lane[1];
+    l1.arena = &ctx->arena1;
+    l1.desc = &ctx->desc1;
+    l1.pin_desc = &ctx->pin_desc1;
+    l1.pin_in = &ctx->pin_in1;
+    l1.pin_out = &ctx->pin_out1;
+    for (cudaStream_t* st : {&l1.s, &l1.s2, &l1.s3})
+      QTNG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    for (cudaEvent_t* ev : {&l1.fork, &l1.join2, &l1.join3})
+      QTNG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     if (arena_bytes) ctx->ensure_arena(arena_bytes / sizeof(double2));
     *out = ctx.release();
   });
@@ -456,13 +487,16 @@ void qtng_destroy(qtng_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->stream2);
   cudaStreamSynchronize(ctx->stream3);
-  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev})
+  const Lane l1 = ctx->lane[1];
+  for (cudaStream_t st : {l1.s, l1.s2, l1.s3})
+    if (st) cudaStreamSynchronize(st);
+  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev, l1.fork,
+                        l1.join2, l1.join3})
     if (e) cudaEventDestroy(e);
   cudaStream_t s = ctx->stream, s2 = ctx->stream2, s3 = ctx->stream3;
-  delete ctx;  // frees the arena and staging buffers
-  if (s) cudaStreamDestroy(s);
-  if (s2) cudaStreamDestroy(s2);
-  if (s3) cudaStreamDestroy(s3);
+  delete ctx;  // frees the arenas and staging buffers
+  for (cudaStream_t st : {s, s2, s3, l1.s, l1.s2, l1.s3})
+    if (st) cudaStreamDestroy(st);
 }
 
 qtng_status qtng_set_precision(qtng_ctx* ctx, int bits) {
@@ -628,6 +662,38 @@ void run_program_once(qtng_ctx* ctx, const HostPlan& hp, const double* input,
     const size_t nb = (hp.lc_begin.size() - 1) * sizeof(double2);
     QTNG_CUDA(cudaMemcpyAsync(terms_host, pr.terms(), nb, cudaMemcpyDeviceToHost, ctx->stream));
   }
+}
+
+// One half of a pipelined energy on `la`: inputs (gate table) and
+// descriptors uploaded, the program enqueued, its terms copied back into the
+// lane's pinned buffer -- all asynchronous on the lane's main stream.
+void enqueue_energy_chunk(qtng_ctx* ctx, Lane& la, bool lane0, const HostPlan& hp,
+                          const double* table) {
+  const DescLayout L = layout_of(hp);
+  const size_t eb = elem_bytes(hp);
+  const uint64_t elems = std::max(hp.arena_elems, hp.input_elems);
+  if (lane0) {
+    ctx->ensure_arena(elems, eb);
+  } else if (std::max<uint64_t>(elems, 32) * eb > la.arena->cap) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (std::max<uint64_t>(elems, 32) * eb > free_b + la.arena->cap)
+      throw Error(kResource, "device arena of " + std::to_string(elems * eb) +
+                                 " bytes exceeds free HBM (" + std::to_string(free_b) + ")");
+    QTNG_CUDA(cudaStreamSynchronize(la.s));
+    la.arena->ensure(std::max<uint64_t>(elems, 32) * eb);
+  }
+  la.desc->ensure(L.total);
+  la.pin_in->ensure(std::max<uint64_t>(hp.input_elems, 1) * eb);
+  stage_input(hp, table, hp.input_elems, la.pin_in->p);
+  QTNG_CUDA(cudaMemcpyAsync(la.arena->p, la.pin_in->p, hp.input_elems * eb, cudaMemcpyHostToDevice,
+                            la.s));
+  upload_desc(ctx, hp, L, static_cast<char*>(la.desc->p), &la);
+  const DevProgram pr{static_cast<char*>(la.desc->p), L, hp.c64};
+  enqueue_program(ctx, hp, pr, la.arena->p, nullptr, nullptr, &la);
+  const size_t nb = (hp.lc_begin.size() - 1) * sizeof(double2);
+  la.pin_out->ensure(std::max<size_t>(nb, 16));
+  QTNG_CUDA(cudaMemcpyAsync(la.pin_out->p, pr.terms(), nb, cudaMemcpyDeviceToHost, la.s));
 }
 
 }  // namespace
@@ -1101,56 +1167,77 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
     const Graph g = graph_from(n, m, edges);
     const std::vector<int> s = selection(m, n_sel, sel);
     PhaseTimer tm("qtng_energy");
-    ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, s);
-    tm.mark("schedules+walks");
-    // cap refusals surface per edge, the first in edge order wins (engine.cpp:543-546)
-    std::vector<const WalkResult*> ok;
-    std::vector<int> ok_idx;
-    int first_fail = -1;
-    for (size_t i = 0; i < cs.walks.size(); ++i) {
-      if (cs.walks[i].fail_code) {
-        if (first_fail < 0) first_fail = static_cast<int>(i);
-      } else {
-        ok.push_back(&cs.walks[i]);
-        ok_idx.push_back(static_cast<int>(i));
-      }
+    // Two lanes: the second half of the lightcones is planned on the host
+    // while the first half runs on the device (QTNG_PIPELINE=0: one program).
+    static const bool pipeline = [] {
+      const char* v = std::getenv("QTNG_PIPELINE");
+      return !(v && v[0] == '0');
+    }();
+    const int K = pipeline && s.size() >= 8 ? 2 : 1;
+    std::vector<std::vector<int>> pos(K), part(K);  // positions in s, edge indices
+    for (size_t i = 0; i < s.size(); ++i) {
+      pos[i % K].push_back(static_cast<int>(i));
+      part[i % K].push_back(s[i]);
     }
-    std::vector<double> t(2 * cs.walks.size(), 0.0);
-    if (!ok.empty()) {
-      HostPlan hp = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
-      hp.c64 = ctx->prec == 64;
+    std::vector<ConeSet> cs(K);
+    std::vector<HostPlan> hps(K);
+    std::vector<std::vector<int>> okpos(K);  // positions (in s) of the contracted lightcones
+    std::vector<const WalkResult*> failed(s.size(), nullptr);
+    std::vector<Edge> edge_at(s.size());
+    std::vector<double> table;
+    std::unique_lock<std::mutex> lk(ctx->mu, std::defer_lock);
+    for (int c = 0; c < K; ++c) {
+      cs[c] = plan_cones(g, p, merged != 0, max_result_width, part[c]);
+      std::vector<const WalkResult*> ok;
+      for (size_t k = 0; k < cs[c].walks.size(); ++k) {
+        edge_at[pos[c][k]] = cs[c].edges[k];
+        if (cs[c].walks[k].fail_code) {
+          failed[pos[c][k]] = &cs[c].walks[k];
+        } else {
+          ok.push_back(&cs[c].walks[k]);
+          okpos[c].push_back(pos[c][k]);
+        }
+      }
+      tm.mark("schedules+walks");
+      if (ok.empty()) continue;
+      hps[c] = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
+      hps[c].c64 = ctx->prec == 64;
       tm.mark("build_plan");
-      std::vector<double> table(2 * hp.input_elems);
-      fill_gate_table(p, gammas, betas, table.data());
-      std::lock_guard<std::mutex> lk(ctx->mu);
-      QTNG_CUDA(cudaSetDevice(ctx->device));
-      run_program_once(ctx, hp, table.data(), hp.input_elems, nullptr);
+      if (table.empty()) {
+        table.resize(2 * hps[c].input_elems);
+        fill_gate_table(p, gammas, betas, table.data());
+      }
+      if (!lk.owns_lock()) {
+        lk.lock();
+        QTNG_CUDA(cudaSetDevice(ctx->device));
+      }
+      enqueue_energy_chunk(ctx, ctx->lane[c], c == 0, hps[c], table.data());
       tm.mark("upload+enqueue");
-      ctx->pin_out.ensure(ok.size() * sizeof(double2));
-      DevProgram pr{static_cast<char*>(ctx->desc.p), layout_of(hp), hp.c64};
-      QTNG_CUDA(cudaMemcpyAsync(ctx->pin_out.p, pr.terms(), ok.size() * sizeof(double2),
-                                cudaMemcpyDeviceToHost, ctx->stream));
-      QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
-      tm.mark("device+d2h");
-      const double* o = static_cast<const double*>(ctx->pin_out.p);
-      for (size_t k = 0; k < ok.size(); ++k) {
-        t[2 * ok_idx[k]] = o[2 * k];
-        t[2 * ok_idx[k] + 1] = o[2 * k + 1];
+    }
+    std::vector<double> t(2 * s.size(), 0.0);
+    for (int c = 0; c < K; ++c) {
+      if (okpos[c].empty()) continue;
+      QTNG_CUDA(cudaStreamSynchronize(ctx->lane[c].s));
+      const double* o = static_cast<const double*>(ctx->lane[c].pin_out->p);
+      for (size_t k = 0; k < okpos[c].size(); ++k) {
+        t[2 * okpos[c][k]] = o[2 * k];
+        t[2 * okpos[c][k] + 1] = o[2 * k + 1];
       }
     }
-    for (size_t i = 0; i < cs.walks.size(); ++i) {
-      const bool refused = cs.walks[i].fail_code != 0;
+    tm.mark("device+d2h");
+    for (size_t i = 0; i < s.size(); ++i) {
+      const bool refused = failed[i] != nullptr;
       const bool complex_term = !refused && std::abs(t[2 * i + 1]) > imag_tol(ctx->prec == 64);
       if (refused || complex_term) {
-        const std::string what = refused ? cs.walks[i].fail_msg
+        const std::string what = refused ? failed[i]->fail_msg
                                          : "edge term has non-real value: imag = " +
                                                std::to_string(t[2 * i + 1]);
-        throw Error(kSchedule, "edge (" + std::to_string(cs.edges[i].u) + ", " +
-                                   std::to_string(cs.edges[i].v) + "): " + what);
+        throw Error(kSchedule, "edge (" + std::to_string(edge_at[i].u) + ", " +
+                                   std::to_string(edge_at[i].v) + "): " + what);
       }
     }
     double sum = 0.0;  // edge order, like engine.cpp:549-551
-    for (size_t i = 0; i < cs.walks.size(); ++i) sum += t[2 * i];
+    for (size_t i = 0; i < s.size(); ++i) sum += t[2 * i];
     if (energy) *energy = 0.5 * static_cast<double>(m) - 0.5 * sum;
     if (terms) std::copy(t.begin(), t.end(), terms);
   });
