@@ -253,9 +253,10 @@ struct qtng_ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, join3_ev = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf sv_scratch;     // state-vector oracle: edge bits, per-edge sums, partials
-  Lane lane[2];          // lane 0 aliases the fields above; lane 1 owns its own
-  DevBuf arena1, desc1;
-  PinBuf pin_desc1, pin_in1, pin_out1;
+  static constexpr int kLanes = 4;
+  Lane lane[kLanes];     // lane 0 aliases the fields above; lanes 1.. own theirs
+  DevBuf arena_x[kLanes], desc_x[kLanes];
+  PinBuf pin_desc_x[kLanes], pin_in_x[kLanes], pin_out_x[kLanes];
   int prec = 128;        // QAOA plans / energies: 128 = complex128, 64 = complex64
 
   // arena of `elems` elements of `elem_bytes` (16: double2, 8: float2)
@@ -466,16 +467,18 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
     Lane& l0 = ctx->lane[0];
     l0 = Lane{ctx->stream, ctx->stream2, ctx->stream3, ctx->fork_ev, ctx->join_ev, ctx->join3_ev,
               &ctx->arena, &ctx->desc, &ctx->pin_desc, &ctx->pin_in, &ctx->pin_out};
-    Lane& l1 = ctx->lane[1];
-    l1.arena = &ctx->arena1;
-    l1.desc = &ctx->desc1;
-    l1.pin_desc = &ctx->pin_desc1;
-    l1.pin_in = &ctx->pin_in1;
-    l1.pin_out = &ctx->pin_out1;
-    for (cudaStream_t* st : {&l1.s, &l1.s2, &l1.s3})
-      QTNG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&l1.fork, &l1.join2, &l1.join3})
-      QTNG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    for (int i = 1; i < qtng_ctx::kLanes; ++i) {
+      Lane& l1 = ctx->lane[i];
+      l1.arena = &ctx->arena_x[i];
+      l1.desc = &ctx->desc_x[i];
+      l1.pin_desc = &ctx->pin_desc_x[i];
+      l1.pin_in = &ctx->pin_in_x[i];
+      l1.pin_out = &ctx->pin_out_x[i];
+      for (cudaStream_t* st : {&l1.s, &l1.s2, &l1.s3})
+        QTNG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+      for (cudaEvent_t* ev : {&l1.fork, &l1.join2, &l1.join3})
+        QTNG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    }
     if (arena_bytes) ctx->ensure_arena(arena_bytes / sizeof(double2));
     *out = ctx.release();
   });
@@ -487,15 +490,21 @@ void qtng_destroy(qtng_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->stream2);
   cudaStreamSynchronize(ctx->stream3);
-  const Lane l1 = ctx->lane[1];
-  for (cudaStream_t st : {l1.s, l1.s2, l1.s3})
-    if (st) cudaStreamSynchronize(st);
-  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev, l1.fork,
-                        l1.join2, l1.join3})
+  std::vector<cudaStream_t> streams = {ctx->stream, ctx->stream2, ctx->stream3};
+  for (int i = 1; i < qtng_ctx::kLanes; ++i) {
+    const Lane& l1 = ctx->lane[i];
+    for (cudaStream_t st : {l1.s, l1.s2, l1.s3})
+      if (st) {
+        cudaStreamSynchronize(st);
+        streams.push_back(st);
+      }
+    for (cudaEvent_t e : {l1.fork, l1.join2, l1.join3})
+      if (e) cudaEventDestroy(e);
+  }
+  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev})
     if (e) cudaEventDestroy(e);
-  cudaStream_t s = ctx->stream, s2 = ctx->stream2, s3 = ctx->stream3;
   delete ctx;  // frees the arenas and staging buffers
-  for (cudaStream_t st : {s, s2, s3, l1.s, l1.s2, l1.s3})
+  for (cudaStream_t st : streams)
     if (st) cudaStreamDestroy(st);
 }
 
@@ -1167,13 +1176,14 @@ qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
     const Graph g = graph_from(n, m, edges);
     const std::vector<int> s = selection(m, n_sel, sel);
     PhaseTimer tm("qtng_energy");
-    // Two lanes: the second half of the lightcones is planned on the host
-    // while the first half runs on the device (QTNG_PIPELINE=0: one program).
-    static const bool pipeline = [] {
-      const char* v = std::getenv("QTNG_PIPELINE");
-      return !(v && v[0] == '0');
+    // K lanes: lightcone chunk c+1 is planned on the host while chunks <= c
+    // run on the device (QTNG_PIPELINE=1: one program).
+    static const int lanes = [] {
+      const char* v = std::getenv("QTNG_PIPELINE");  // lanes (1 = no pipelining)
+      const int x = v ? std::atoi(v) : 3;
+      return std::max(1, std::min(x, qtng_ctx::kLanes));
     }();
-    const int K = pipeline && s.size() >= 8 ? 2 : 1;
+    const int K = std::max(1, std::min<int>(lanes, static_cast<int>(s.size()) / 4));
     std::vector<std::vector<int>> pos(K), part(K);  // positions in s, edge indices
     for (size_t i = 0; i < s.size(); ++i) {
       pos[i % K].push_back(static_cast<int>(i));
