@@ -54,3 +54,19 @@ def test_c2_headline_two_methods(q, ctx, golden):
     assert abs(e - c["energy_naive"]) <= 1e-10 * abs(c["energy_naive"])
     terms = np.array([x for x, _ in c["terms_naive"]])
     assert np.max(np.abs(zz - terms)) <= 1e-10
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_instances_two_methods(q, ctx, seed):
+    # random graphs and angles: the bucket-elimination energy (fused chains,
+    # pipelined one-shot path) against the device state vector
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([6, 8, 10, 12, 14, 16]))
+    p = int(rng.integers(1, 4))
+    g = q.random_regular(n, 3, int(rng.integers(0, 1 << 30)))
+    a = q.Angles(list(rng.uniform(-np.pi, np.pi, p)), list(rng.uniform(-np.pi, np.pi, p)))
+    res = q.energy_expectation(g, a, q.GpuBackend(ctx))
+    e_sv, zz = q.statevector_energy(g, a, ctx=ctx)
+    assert abs(res.energy - e_sv) <= 1e-10 * max(1.0, abs(e_sv)), (n, p)
+    assert np.max(np.abs(res.terms.real - zz)) <= 1e-10
+    assert np.max(np.abs(res.terms.imag)) <= 1e-8
