@@ -36,7 +36,7 @@ class Pool {
       n_ = n;
       next_.store(0);
       active_ = static_cast<int>(workers_.size());
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     drain();
@@ -54,7 +54,7 @@ class Pool {
     {
       std::lock_guard<std::mutex> lk(mu_);
       stop_ = true;
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     for (auto& t : workers_) t.join();
@@ -65,10 +65,17 @@ class Pool {
   void loop() {
     uint64_t seen = 0;
     for (;;) {
+      // spin briefly first: the planner issues several loops back to back and
+      // a futex wake-up per loop would cost more than the loop itself
+      bool woke = false;
+      for (int k = 0; k < kSpin && !woke; ++k) {
+        woke = gen_.load(std::memory_order_acquire) != seen;
+        if (!woke) std::this_thread::yield();
+      }
       {
         std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
+        cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+        seen = gen_.load(std::memory_order_acquire);
         if (stop_) return;
       }
       drain();
@@ -85,7 +92,8 @@ class Pool {
   int n_ = 0;
   std::atomic<int> next_{0};
   int active_ = 0;
-  uint64_t gen_ = 0;
+  std::atomic<uint64_t> gen_{0};
+  static constexpr int kSpin = 2000;  // yields before sleeping on the condition variable
   bool stop_ = false;
 };
 
