@@ -102,6 +102,10 @@ const char* qtng_last_error(void);
 /* Library build string (arch, version). */
 const char* qtng_version(void);
 
+/* Kernel launches the library has issued since it was loaded (eager launches
+ * when enqueued; graph replays as kernels per graph x replays). */
+uint64_t qtng_kernel_launches(void);
+
 /* ---------------------------------------------------------------- host side */
 
 /* random_regular (proj/src/graph.cpp:45-76): edges written to edges[2*m];

@@ -67,6 +67,11 @@ def _check(status: int) -> None:
         raise _ERRORS.get(status, RuntimeError)(lib.qtng_last_error().decode())
 
 
+def kernel_launches() -> int:
+    """Kernel launches the native library has issued (eager + graph replays)."""
+    return int(lib.qtng_kernel_launches())
+
+
 def version() -> str:
     return lib.qtng_version().decode()
 

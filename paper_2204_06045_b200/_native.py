@@ -79,6 +79,8 @@ def _load():
                                       C.POINTER(C.c_float)]
     lib.qtng_plan_run_device.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
     lib.qtng_plan_info_get.argtypes = [vp, C.POINTER(PlanInfo)]
+    lib.qtng_kernel_launches.argtypes = []
+    lib.qtng_kernel_launches.restype = C.c_uint64
     lib.qtng_set_precision.argtypes = [vp, C.c_int]
     lib.qtng_statevector_energy.argtypes = [vp, C.c_int, C.c_int, i32p, C.c_int, f64p, f64p,
                                             C.c_int, C.POINTER(C.c_double), C.c_void_p]
@@ -103,6 +105,6 @@ EXPORTED = [
     "qtng_create", "qtng_destroy", "qtng_last_error", "qtng_version", "qtng_random_regular",
     "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_edge_work", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
     "qtng_contract_schedule", "qtng_energy", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute",
-    "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_set_precision", "qtng_statevector_energy", "qtng_plan_segments", "qtng_plan_records", "qtng_plan_level_ms", "qtng_plan_kernel_ms",
+    "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_kernel_launches", "qtng_set_precision", "qtng_statevector_energy", "qtng_plan_segments", "qtng_plan_records", "qtng_plan_level_ms", "qtng_plan_kernel_ms",
     "qtng_plan_destroy", "qtng_plan_time_level",
 ]

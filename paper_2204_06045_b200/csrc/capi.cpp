@@ -37,6 +37,11 @@ thread_local std::string g_err;
       throw Error(kCuda, std::string(#call) + ": " + cudaGetErrorString(e_));            \
   } while (0)
 
+// Kernel launches issued by the library (eager launches as they are
+// enqueued, graph replays as kernels-per-graph x replays): the evidence
+// behind bench.py's gpu_launches.
+std::atomic<uint64_t> g_launches{0};
+
 // QTNG_TIMING=1: host phase times of the one-shot calls on stderr (tuning aid).
 struct PhaseTimer {
   const char* name;
@@ -357,17 +362,24 @@ void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* d
   pack_desc(hp, L, static_cast<char*>(la.pin_desc->p));
   QTNG_CUDA(cudaMemcpyAsync(dev, la.pin_desc->p, L.upload, cudaMemcpyHostToDevice, la.s));
   const DevProgram pr{dev, L, hp.c64};
+  if (!hp.segs.empty()) g_launches.fetch_add(1, std::memory_order_relaxed);
   QTNG_CUDA(c128::launch_seg_prep(la.s, pr.segs(), static_cast<uint32_t>(hp.segs.size()), pr.trefs(),
                             pr.segtab()));
 }
 
 // Enqueue the whole program on the context's stream: every level, then the
 // per-lightcone products.
+int launches_per_run(const HostPlan& hp);
+
 void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, void* arena,
                      std::vector<cudaEvent_t>* level_events,
                      std::vector<cudaEvent_t>* kernel_events = nullptr, const Lane* ln = nullptr) {
   const Lane& la = ln ? *ln : ctx->lane[0];
   cudaStream_t s = la.s;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  QTNG_CUDA(cudaStreamIsCapturing(s, &cap));
+  if (cap == cudaStreamCaptureStatusNone)
+    g_launches.fetch_add(static_cast<uint64_t>(launches_per_run(hp)), std::memory_order_relaxed);
   if (hp.flow) {  // one persistent dataflow kernel instead of the level sequence
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[0], s));
     const DescLayout& L = pr.L;
@@ -445,6 +457,8 @@ struct qtng_plan {
 extern "C" {
 
 const char* qtng_last_error(void) { return g_err.c_str(); }
+
+uint64_t qtng_kernel_launches(void) { return g_launches.load(); }
 
 const char* qtng_version(void) {
   return "qtng 0.1 (sm_100a level-batched bucket elimination, complex128, bit-exact naive order)";
@@ -948,6 +962,8 @@ qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms) 
     }
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
     for (int i = 0; i < n_runs; ++i) QTNG_CUDA(cudaGraphLaunch(plan->graph, ctx->stream));
+    g_launches.fetch_add(static_cast<uint64_t>(launches_per_run(hp)) * static_cast<uint64_t>(n_runs),
+                         std::memory_order_relaxed);
     QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;
