@@ -80,6 +80,16 @@ int seg_max_j() {
   return j;
 }
 
+// Levels whose segments have fewer tiles than this put digits on lanes
+// (QTNG_SEG_STARVED, default 1024).
+uint64_t seg_starved_tiles() {
+  static const uint64_t t = [] {
+    const char* v = std::getenv("QTNG_SEG_STARVED");
+    return static_cast<uint64_t>(v ? std::atoll(v) : 1024);
+  }();
+  return t;
+}
+
 bool flow_default() {
   static const bool on = [] {
     const char* v = std::getenv("QTNG_FLOW");
@@ -215,11 +225,12 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   // stable counting sort of units by level; release lists by consumer level
   std::vector<uint32_t> lstart(n_levels + 1, 0), order(U);
   std::vector<uint32_t> rstart(n_levels + 1, 0), rel;
-  std::vector<uint64_t> level_rows(n_levels, 0);
+  std::vector<uint64_t> level_rows(n_levels, 0), level_tiles(n_levels, 0);
   for (uint32_t u = 0; u < U; ++u) {
     ++lstart[unit_level[u] + 1];
     const Op& o = op_at(unit_last[u]);
     if (unit_len[u] == 1) level_rows[unit_level[u]] += o.r > 5 ? uint64_t{1} << (o.r - 5) : 1;
+    else level_tiles[unit_level[u]] += o.r > kSegYBits ? uint64_t{1} << (o.r - kSegYBits) : 1;
     const int64_t cu = consumer_unit(u);
     if (cu >= 0) ++rstart[unit_level[cu] + 1];
   }
@@ -260,6 +271,19 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     while (row_bits < kItemBits - 5 && (level_rows[L] >> (row_bits + 1)) >= kTargetItems) ++row_bits;
     level_cb[L] = 5 + row_bits;
   }
+  // Y bits on the lanes of a segment tile: 5, unless the level's segments
+  // have too few tiles to occupy the GPU (small plans, one GPU's shard of a
+  // few lightcones) -- then fewer Y bits and the lowest digits move onto the
+  // freed lanes (shorter serial digit walks per tile)
+  std::vector<int> level_cy(n_levels, kSegYBits);
+  for (int L = 0; L < n_levels; ++L) {
+    int h = 0;
+    while (h < kSegYBits && level_tiles[L] && (level_tiles[L] << h) < seg_starved_tiles()) ++h;
+    level_cy[L] = kSegYBits - h;
+  }
+  auto seg_cy = [&](uint32_t u) {
+    return std::min<int>(op_at(unit_last[u]).r, level_cy[unit_level[u]]);
+  };
   // outer-join classification of single-op units (DevOp::lead/rb), in parallel
   std::vector<uint32_t> outer_sig(N, 0);  // 0 = generic; else 1 | lead<<8 | rb0<<16 | rb1<<24
   {
@@ -348,7 +372,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
           ist += unit_len[u];
           sg.nst = static_cast<uint8_t>(unit_len[u]);
           sg.ry = static_cast<uint8_t>(o.r);
-          sg.cy = static_cast<uint8_t>(std::min<int>(o.r, kSegYBits));
+          sg.cy = static_cast<uint8_t>(seg_cy(u));
           sg.nops = static_cast<uint8_t>(unit_nops[u]);
           sg.item_begin = ll.seg_items;
           hp.seg_ibeg[is - 1] = ll.seg_items;
@@ -410,7 +434,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       ++stamp;
       // var -> code.  Single op: output bit (LSB-indexed) / kSumSrc + j.
       // Segment: Y bit -> in-tile or tile-number bit; digit s_k -> in-tile bit
-      const int ry = last.r, cy = std::min<int>(ry, kSegYBits);
+      const int ry = last.r, cy = seg ? seg_cy(u) : 0;
       const int32_t* ov = w.out_vars(last);
       for (int k = 0; k < ry; ++k) {
         const int b = ry - 1 - k;

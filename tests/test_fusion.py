@@ -61,7 +61,7 @@ def test_segment_shapes(q, golden):
     levels = [s["level"] for s in segs]
     assert levels == sorted(levels)
     for s in segs:
-        assert 2 <= s["L"] <= 9 and s["cy"] == min(s["ry"], 5)
+        assert 2 <= s["L"] <= 9 and 0 <= s["cy"] <= min(s["ry"], 5)
         assert s["nops"] == sum(st[0] for st in s["stages"]) <= 16
         nt1, ns1, main1, _ = s["stages"][0]
         assert main1 == -1 and ns1 <= 1 and nt1 <= 6
