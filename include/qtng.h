@@ -223,7 +223,8 @@ qtng_status qtng_statevector_energy(qtng_ctx* ctx, int n, int m, const int* edge
                                     double* energy, double* zz);
 
 /* Host-only analysis of the fused-chain segments of the plan for all m
- * edges.  Per segment (level-sorted): level, L (stages), rY, cY, nops; then
+ * edges.  Per segment (level-sorted): level, L (stages), rY, cY, nops, rb
+ * (paired rows: the tile bit of the second row, 255 = unpaired); then
  * per stage: nt, ns, main (-1 for stage 1), and per member: rank,
  * initial (1 = gate / input-region tensor; a main placeholder has rank 0),
  * then its rank axis codes (device_plan.hpp: lane / digit / tile / summed bit).

@@ -488,7 +488,8 @@ def plan_stats(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfi
 def plan_segments(g: Graph, p: int, merged: bool = False,
                   cfg: Optional[EngineConfig] = None) -> List[dict]:
     """Host-only description of the fused-chain segments of Plan(g, p):
-    level, L, ry, cy, nops, stages=[(nt, ns, main, [(rank, initial, codes)])]."""
+    level, L, ry, cy, nops, rb (paired rows' tile bit or None),
+    stages=[(nt, ns, main, [(rank, initial, codes)])]."""
     cfg = cfg or EngineConfig()
     n_ints = C.c_int64(0)
     probe = np.zeros(1, np.int32)
@@ -499,8 +500,8 @@ def plan_segments(g: Graph, p: int, merged: bool = False,
                                   buf, len(buf), C.byref(n_ints)))
     out, i = [], 0
     while i < n_ints.value:
-        lv, L, ry, cy, nops = (int(x) for x in buf[i:i + 5])
-        i += 5
+        lv, L, ry, cy, nops, rb = (int(x) for x in buf[i:i + 6])
+        i += 6
         stages = []
         for _ in range(L):
             nt, ns, main = (int(x) for x in buf[i:i + 3])
@@ -511,7 +512,8 @@ def plan_segments(g: Graph, p: int, merged: bool = False,
                 mem.append((rank, ini, [int(x) for x in buf[i + 2:i + 2 + rank]]))
                 i += 2 + rank
             stages.append((nt, ns, main, mem))
-        out.append(dict(level=lv, L=L, ry=ry, cy=cy, nops=nops, stages=stages))
+        out.append(dict(level=lv, L=L, ry=ry, cy=cy, nops=nops,
+                        rb=None if rb == 0xff else rb, stages=stages))
     return out
 
 

@@ -1017,7 +1017,7 @@ qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged
     for (size_t L = 0; L < hp.levels.size(); ++L)
       for (uint32_t k = 0; k < hp.levels[L].seg_count; ++k) {
         const DevSeg& sg = hp.segs[hp.levels[L].seg_begin + k];
-        out.insert(out.end(), {static_cast<int>(L), sg.nst, sg.ry, sg.cy, sg.nops});
+        out.insert(out.end(), {static_cast<int>(L), sg.nst, sg.ry, sg.cy, sg.nops, sg.rb});
         for (int i = 0; i < sg.nst; ++i) {
           const DevStage& st = hp.stages[sg.stage + i];
           out.insert(out.end(), {st.nt, st.ns, st.main == kSegMain ? -1 : st.main});

@@ -84,6 +84,10 @@ constexpr int kSegMaxStages = kSegMaxJ + 1;
 constexpr int kSegMaxOps = 16;       // operands per segment (all stages)
 constexpr int kSegMaxNt1 = 6;        // members of stage 1
 constexpr int kSegMaxNt = 4;         // members of a fused stage (incl. the main)
+#ifndef QTNG_SEG_PAIR_MAXNT
+#define QTNG_SEG_PAIR_MAXNT 4
+#endif
+constexpr int kSegPairMaxNt = QTNG_SEG_PAIR_MAXNT;  // paired rows only for stage-1 member counts up to this
 constexpr uint8_t kSegMain = 0xff;   // DevStage::main of stage 1 (no main)
 constexpr uint8_t kLaneSrcEnd = 5;
 constexpr uint8_t kJSrc = 8;
@@ -98,6 +102,13 @@ struct alignas(16) DevSeg {
   uint8_t ry;           // rank of Y
   uint8_t cy;           // in-tile Y bits
   uint8_t nops;         // DevTensors of the segment (mains included as placeholders)
+  // Paired rows (cY = 5 only): a lane computes two Y rows, the tile number's
+  // bit rb = 0 and = 1, sharing the digit walk, the side products and the
+  // climb's control; rb is a tile bit that no side member (stage >= 2) reads,
+  // so the side products are the same for both rows.  kNoVar: unpaired.  A
+  // paired segment has half as many work items (tiles with bit rb removed).
+  uint8_t rb;
+  uint8_t pad[7];
 };
 static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
 

@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(kThreads, MAXT <= 2 ? QTNG_MINB_T2 : (MAXT <= 
 level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
              const DevTensor* __restrict__ trefs, V* __restrict__ arena,
              uint32_t op_count, uint32_t items) {
+#ifdef QTNG_NOOP_LEVEL  // launch-floor experiments only (tools/tune.py)
+  return;
+#endif
   __shared__ DevTensor slots[kWarpsPerCta][MAXT];
   __shared__ uint32_t sbeg[kSmemOps];
   // cache the item table in shared memory only when each warp will look it
@@ -369,6 +372,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
              const DevTensor* __restrict__ trefs, V* __restrict__ arena,
              uint32_t op_count, uint32_t items) {
+#ifdef QTNG_NOOP_LEVEL  // launch-floor experiments only (tools/tune.py)
+  return;
+#endif
   __shared__ DevTensor slots[kWarpsPerCta][4];
   __shared__ uint32_t sbeg[kSmemOps];
   // cache the item table in shared memory only when each warp will look it
@@ -475,6 +481,8 @@ struct ChainWarp {
   uint32_t sdesc[kSegMaxStages];
   uint8_t slane[kSegMaxStages][32];      // per lane: the lane bits of the table index
   V acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
+  V acc1[kSegMaxStages - 2][32];   // ... of the second row (paired segments)
+  uint32_t drow[kSegMaxNt1];       // paired: stage-1 member offset of the second row
 };
 
 // (r, 0) * y and p * (r, 0): equal to cmul up to the sign of an exact zero.
@@ -544,6 +552,107 @@ __device__ __forceinline__ V chain_term(const ChainWarp& cw, const SegOpTab* __r
   bool real;
   const V p = chain_side(cw, tab, arena, st.op0, m, j, lane, &real);
   return real ? rscale(p.x, v) : cmul(p, v);
+}
+
+// chain_term for both rows of a paired tile: the side product P_i does not
+// depend on the row bit, so it is looked up or gathered once.
+__device__ __forceinline__ void chain_term2(const ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                            const V* __restrict__ arena, const DevStage st,
+                                            int k, uint32_t j, V& v0, V& v1, int lane) {
+  const uint32_t d = cw.sdesc[k + 1];
+  const uint32_t mode = d & 3u;
+  if (mode == 0) return;
+  V p;
+  bool real;
+  if (mode != 3) {
+    const uint32_t idx = cw.slane[k + 1][lane] | ((j >> k) & 1u) |
+                         (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
+                         (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
+    p = cw.ptab[k + 1][idx];
+    real = mode == 2;
+  } else {
+    p = chain_side(cw, tab, arena, st.op0, st.nt - 1, j, lane, &real);
+  }
+  if (real) {
+    v0 = rscale(p.x, v0);
+    v1 = rscale(p.x, v1);
+  } else {
+    v0 = cmul(p, v0);
+    v1 = cmul(p, v1);
+  }
+}
+
+// One paired tile (DevSeg::rb): chain_tile's walk with U = 1 for two Y rows
+// at once.  Row 1's stage-1 operands sit drow[t] further; everything else
+// (digit offsets, side products, climb control) is shared.  Each row sees
+// exactly the operation sequence of the unpaired walk.
+template <int NT, int NS, int K0>
+__device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __restrict__ tab,
+                                            const DevSeg& sg, V* __restrict__ arena,
+                                            uint32_t tile, int lane) {
+  const int L = sg.nst;
+  const uint32_t nj = 1u << (L - 1);
+  const V* B[NT];
+  uint32_t o[NT], sdl[NT], d0[NT], dr[NT];
+  const R r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : 0.0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    B[t] = arena + __ldg(&tab[t].off);
+    o[t] = cw.toff[t] + __ldg(&tab[t].llane[lane]);
+    sdl[t] = __ldg(&tab[t].sd);
+    d0[t] = __ldg(&tab[t].dj[0]);
+    dr[t] = cw.drow[t];
+  }
+  const DevStage st2 = cw.st[1];
+  V* y = arena + sg.out + (static_cast<uint64_t>(tile) << kSegYBits) + lane;
+  const uint64_t y1 = uint64_t{1} << (sg.rb + kSegYBits);
+  for (uint32_t j = 0; j < nj; j += 2) {
+    if (j) {
+      const int b = __ffs(j) - 1;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t];
+    }
+    V v[2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        uint32_t oq[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) oq[t] = o[t] + (q ? d0[t] : 0u) + (r ? dr[t] : 0u);
+        V x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
+#pragma unroll
+        for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
+        if (NS) {
+          V p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
+#pragma unroll
+          for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
+          x = cadd(x, p);
+        }
+        v[q][r] = x;
+      }
+    }
+    chain_term2(cw, tab, arena, st2, 0, j, v[0][0], v[0][1], lane);
+    chain_term2(cw, tab, arena, st2, 0, j | 1u, v[1][0], v[1][1], lane);
+    V x0 = cadd(v[0][0], v[1][0]), x1 = cadd(v[0][1], v[1][1]);
+    const uint32_t jj = j | 1u;
+    bool carry = true;
+    for (int k = 1; k + 2 <= L; ++k) {
+      chain_term2(cw, tab, arena, cw.st[k + 1], k, jj, x0, x1, lane);
+      if (!((jj >> k) & 1u)) {
+        cw.acc[k - 1][lane] = x0;
+        cw.acc1[k - 1][lane] = x1;
+        carry = false;
+        break;
+      }
+      x0 = cadd(cw.acc[k - 1][lane], x0);
+      x1 = cadd(cw.acc1[k - 1][lane], x1);
+    }
+    if (carry) {
+      y[0] = x0;
+      y[y1] = x1;
+    }
+  }
 }
 
 // One tile: 2^J stage-1 evaluations (NT members, NS summed bits), in groups
@@ -720,6 +829,13 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
     else chain_tile_lanes<NT, NS, 0>(cw, tab, sg, arena, tile, lane);
     return;
   }
+  if constexpr (NT <= kSegPairMaxNt) {
+    if (sg.rb != kNoVar) {  // paired rows
+      if (k0) chain_tile2<NT, NS, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+      else chain_tile2<NT, NS, 0>(cw, tab, sg, arena, tile, lane);
+      return;
+    }
+  }
   constexpr int U = NT <= QTNG_SEG_U2_MAXNT ? 2 : 1;  // groups of 2^U digit values
   if (U == 2 && sg.nst >= 3) {
     if (k0) chain_tile<NT, NS, U, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
@@ -821,12 +937,16 @@ __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const D
 }
 
 // One tile of the loaded segment.
-__device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t tile,
+__device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t item,
                                          const DevTensor* __restrict__ trefs,
                                          const SegOpTab* __restrict__ segtab,
                                          V* __restrict__ arena, int lane) {
   const DevSeg& sg = sc.sg;
   const SegOpTab* tab = segtab + sg.tref;
+  // paired: the work item is the tile number without bit rb (row 0 = bit clear)
+  const bool paired = sg.rb != kNoVar;
+  const uint32_t tile = paired ? insert_zero(item, sg.rb) : item;
+  if (paired && lane < kSegMaxNt1 && lane < sg.nops) cw.drow[lane] = __ldg(&tab[lane].dtile[sg.rb]);
   for (int op = 0; op < sg.nops; ++op) {
     const uint32_t v = ((tile >> lane) & 1u) ? __ldg(&tab[op].dtile[lane]) : 0u;
     const uint32_t sum = __reduce_add_sync(kFull, v);
@@ -860,15 +980,23 @@ __device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t 
 }
 
 #ifndef QTNG_SEG_MINB
-#define QTNG_SEG_MINB 32  // resident one-warp CTAs per SM (tuned: 32 = the per-SM block limit)
+#define QTNG_SEG_MINB 28  // resident seg_kernel warps per SM the register budget must allow (72 regs)
 #endif
-__global__ void __launch_bounds__(32, QTNG_SEG_MINB)
+#ifndef QTNG_SEG_WARPS
+#define QTNG_SEG_WARPS 1  // warps per CTA (independent; fewer CTAs = less reserved shared memory)
+#endif
+constexpr int kSegWarps = QTNG_SEG_WARPS;
+__global__ void __launch_bounds__(32 * kSegWarps, QTNG_SEG_MINB / kSegWarps)
 seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
            const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
            const SegOpTab* __restrict__ segtab, V* __restrict__ arena, uint32_t seg_count,
            uint32_t items, uint32_t* ctr) {
-  __shared__ ChainWarp cw;
-  const int lane = threadIdx.x;
+#ifdef QTNG_NOOP_SEG  // launch-floor experiments only (tools/tune.py)
+  return;
+#endif
+  __shared__ ChainWarp cws[kSegWarps];
+  ChainWarp& cw = cws[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
   // dynamic tile queue (segments are sorted by per-tile cost, largest first);
   // ctr[0] = next tile, ctr[1] = finished warps; the last warp resets both
   SegCursor sc;
@@ -893,7 +1021,7 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
   }
   if (lane == 0) {
     __threadfence();
-    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every warp has left the queue
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x * kSegWarps - 1) {  // every warp has left the queue
       ctr[0] = 0;
       ctr[1] = 0;
     }
@@ -1013,10 +1141,11 @@ int seg_grid(uint32_t items) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_kernel, 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_kernel, 32 * kSegWarps, 0);
     cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  return static_cast<int>(items < static_cast<uint32_t>(cap) ? (items > 0 ? items : 1) : cap);
+  const uint32_t ctas = (items + kSegWarps - 1) / kSegWarps;
+  return static_cast<int>(ctas < static_cast<uint32_t>(cap) ? (ctas > 0 ? ctas : 1) : cap);
 }
 
 // Per lightcone: e_jk = prod of its scalar results in production order
@@ -1116,7 +1245,7 @@ cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_
                         void* arena_v, uint32_t* ctr, const LevelLaunch& lv) {
   if (lv.seg_items == 0) return cudaSuccess;
   V* arena = static_cast<V*>(arena_v);
-  seg_kernel<<<seg_grid(lv.seg_items), 32, 0, s>>>(
+  seg_kernel<<<seg_grid(lv.seg_items), 32 * kSegWarps, 0, s>>>(
       segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, trefs, segtab, arena, lv.seg_count,
       lv.seg_items, ctr);
   return cudaGetLastError();

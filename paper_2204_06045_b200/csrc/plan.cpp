@@ -82,6 +82,25 @@ int seg_max_j() {
 
 // Levels whose segments have fewer tiles than this put digits on lanes
 // (QTNG_SEG_STARVED, default 1024).
+// Segments of levels with at least this many tiles pair their rows
+// (DevSeg::rb; QTNG_SEG_PAIR, default 8192; 0 disables pairing).
+uint64_t seg_pair_min_tiles() {
+  static const uint64_t t = [] {
+    const char* v = std::getenv("QTNG_SEG_PAIR");
+    return static_cast<uint64_t>(v ? std::atoll(v) : 8192);
+  }();
+  return t;
+}
+
+// Stage-1 member counts paired (QTNG_SEG_PAIR_NT, at most kSegPairMaxNt).
+int seg_pair_max_nt() {
+  static const int t = [] {
+    const char* v = std::getenv("QTNG_SEG_PAIR_NT");
+    return std::min(v ? std::atoi(v) : kSegPairMaxNt, kSegPairMaxNt);
+  }();
+  return t;
+}
+
 uint64_t seg_starved_tiles() {
   static const uint64_t t = [] {
     const char* v = std::getenv("QTNG_SEG_STARVED");
@@ -374,6 +393,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
           sg.ry = static_cast<uint8_t>(o.r);
           sg.cy = static_cast<uint8_t>(seg_cy(u));
           sg.nops = static_cast<uint8_t>(unit_nops[u]);
+          sg.rb = kNoVar;  // chosen with the operand maps below
           sg.item_begin = ll.seg_items;
           hp.seg_ibeg[is - 1] = ll.seg_items;
           const uint64_t tiles = uint64_t{1} << (o.r - sg.cy);
@@ -516,10 +536,44 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       if (!seg) {
         DevOp& d = hp.ops[unit_slot[u]];
         mark_invariant_lead(d, hp.trefs.data() + d.tref);
+      } else if (cy == kSegYBits && ry > cy && seg_pair_min_tiles() &&
+                 hp.stages[unit_stage[u]].nt <= seg_pair_max_nt() &&
+                 level_tiles[unit_level[u]] >= seg_pair_min_tiles()) {
+        // paired rows: a tile bit no side member reads, preferring one that
+        // few stage-1 members read (their second-row loads differ)
+        DevSeg& sg = hp.segs[unit_slot[u]];
+        const DevStage* sts = hp.stages.data() + unit_stage[u];
+        uint32_t side = 0, n1[32] = {};
+        for (int i = 0; i < sg.nst; ++i)
+          for (int t = 0; t < sts[i].nt; ++t) {
+            if (i > 0 && t == sts[i].main) continue;
+            const DevTensor& x = hp.trefs[unit_tref[u] + sts[i].op0 + t];
+            for (int ax = 0; ax < x.rank; ++ax) {
+              const uint8_t c = x.src[ax];
+              if (c < kTileSrc || c >= kSumSrc) continue;
+              if (i > 0) side |= 1u << (c - kTileSrc);
+              else ++n1[c - kTileSrc];
+            }
+          }
+        int best = -1;
+        for (int b = 0; b < ry - cy; ++b)
+          if (!((side >> b) & 1u) && (best < 0 || n1[b] < n1[best])) best = b;
+        if (best >= 0) sg.rb = static_cast<uint8_t>(best);
       }
       unit_dev_bytes[u] = dev_bytes;
     }
   });
+  // segment work items (tiles; half as many for paired segments), per level
+  for (LevelLaunch& ll : hp.levels) {
+    ll.seg_items = 0;
+    for (uint32_t k = ll.seg_begin; k < ll.seg_begin + ll.seg_count; ++k) {
+      DevSeg& sg = hp.segs[k];
+      const uint64_t tiles = uint64_t{1} << (sg.ry - sg.cy - (sg.rb != kNoVar ? 1 : 0));
+      sg.item_begin = ll.seg_items;
+      hp.seg_ibeg[k] = ll.seg_items;
+      ll.seg_items += static_cast<uint32_t>(tiles);
+    }
+  }
   for (int e : chunk_err) {
     if (e == 1) throw Error(kResource, "tensor rank exceeds the device limit " + std::to_string(kMaxRank));
     if (e == 2) throw Error(kSchedule, "internal: operand var outside its bucket");
@@ -564,7 +618,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       f.idx = unit_slot[u];
       if (f.kind) {
         const DevSeg& sg = hp.segs[f.idx];
-        f.n_items = 1u << (sg.ry - sg.cy);
+        f.n_items = 1u << (sg.ry - sg.cy - (sg.rb != kNoVar ? 1 : 0));
       } else {
         const DevOp& d = hp.ops[f.idx];
         f.n_items = 1u << (d.r - d.cb);

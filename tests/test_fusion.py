@@ -70,6 +70,25 @@ def test_segment_shapes(q, golden):
             assert mem[main][0] == 0  # placeholder: read from registers
             assert all(rank > 0 for rank, _, _ in mem[:main])
         # stage i's result rank shrinks by its summed var: rY = r_1 - (L - 1)
+        if s["rb"] is not None:
+            # paired rows: full lane tiles, a tile bit that no side member reads
+            assert s["cy"] == 5 and 0 <= s["rb"] < s["ry"] - 5 and nt1 <= 4
+            for nt, ns, main, mem in s["stages"][1:]:
+                for t, (rank, _, codes) in enumerate(mem):
+                    assert t == main or 32 + s["rb"] not in codes
+    assert any(s["rb"] is not None for s in segs)
+
+
+def test_pairing_switch(q, golden):
+    # QTNG_SEG_PAIR=0 disables paired rows (read once per process: child)
+    c, p = _cfg(golden, "C2")
+    code = ("import sys; sys.path.insert(0, %r); import paper_2204_06045_b200 as q; "
+            "g = q.random_regular(%d, 3, %d); "
+            "print(sum(s['rb'] is not None for s in q.plan_segments(g, %d)))") % (ROOT, c["n"], c["seed"], p)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, QTNG_SEG_PAIR="0"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert int(r.stdout.strip().splitlines()[-1]) == 0
 
 
 def _child_energy(name, env):
@@ -97,10 +116,11 @@ def test_fused_equals_unfused_bitwise(golden, name):
     ref = np.array([complex(x, y) for x, y in golden["configs"][name]["terms_naive"]])
     plain = _child_energy(name, {"QTNG_FUSE": "0"})
     assert plain["segments"] == 0
-    for j in ("1", "3", "8"):
-        fused = _child_energy(name, {"QTNG_SEG_J": j})
+    for env in ({"QTNG_SEG_J": "1"}, {"QTNG_SEG_J": "3"}, {"QTNG_SEG_J": "8"},
+                {"QTNG_SEG_PAIR": "0"}, {"QTNG_SEG_PAIR": "1"}, {"QTNG_SEG_PAIR_NT": "2"}):
+        fused = _child_energy(name, env)
         assert fused["segments"] > 0
-        assert fused["terms"] == plain["terms"], f"QTNG_SEG_J={j}"
+        assert fused["terms"] == plain["terms"], str(env)
     got = np.array([complex(x, y) for x, y in plain["terms"]])
     assert np.array_equal(got, ref)
 
