@@ -473,13 +473,13 @@ __global__ void seg_prep_kernel(const DevSeg* __restrict__ segs, uint32_t n_segs
 struct ChainWarp {
   uint32_t toff[kSegMaxOps];             // tile part of each operand's offset
   DevStage st[kSegMaxStages];
-  V ptab[kSegMaxStages][8];        // tabulated side products P_i(s_i, u0, u1) of this tile
+  V ptab[kSegMaxStages - 1][8];    // [i - 1]: tabulated side products P_i(s_i, u0, u1) of this tile
   uint8_t preal[kSegMaxStages];          // 1: P_i is a real scalar (scale instead of multiply)
   // per stage: bits 0-1 mode (0 no side member, 1 table, 2 real table, 3
   // gathered), bits 8-12 / 13 and 16-20 / 21: digit position / valid of the
   // table index bits 1 and 2
   uint32_t sdesc[kSegMaxStages];
-  uint8_t slane[kSegMaxStages][32];      // per lane: the lane bits of the table index
+  uint8_t slane[kSegMaxStages - 1][32];  // [i - 1], per lane: the lane bits of the table index
   V acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
   V acc1[kSegMaxStages - 2][32];   // ... of the second row (paired segments)
   uint32_t drow[kSegMaxNt1];       // paired: stage-1 member offset of the second row
@@ -542,10 +542,10 @@ __device__ __forceinline__ V chain_term(const ChainWarp& cw, const SegOpTab* __r
   const uint32_t mode = d & 3u;
   if (mode == 0) return v;
   if (mode != 3) {
-    const uint32_t idx = cw.slane[k + 1][lane] | ((j >> k) & 1u) |
+    const uint32_t idx = cw.slane[k][lane] | ((j >> k) & 1u) |
                          (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
                          (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
-    const V p = cw.ptab[k + 1][idx];
+    const V p = cw.ptab[k][idx];
     return mode == 2 ? rscale(p.x, v) : cmul(p, v);
   }
   const int m = st.nt - 1;
@@ -565,10 +565,10 @@ __device__ __forceinline__ void chain_term2(const ChainWarp& cw, const SegOpTab*
   V p;
   bool real;
   if (mode != 3) {
-    const uint32_t idx = cw.slane[k + 1][lane] | ((j >> k) & 1u) |
+    const uint32_t idx = cw.slane[k][lane] | ((j >> k) & 1u) |
                          (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
                          (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
-    p = cw.ptab[k + 1][idx];
+    p = cw.ptab[k][idx];
     real = mode == 2;
   } else {
     p = chain_side(cw, tab, arena, st.op0, st.nt - 1, j, lane, &real);
@@ -882,7 +882,7 @@ __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
           pr = false;
         }
       }
-      cw.ptab[i][e] = p;
+      cw.ptab[i - 1][e] = p;
     }
   }
 }
@@ -924,12 +924,12 @@ __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const D
     cw.sdesc[lane] = d;
   }
   __syncwarp();
-  for (int i = 0; i < sg.nst; ++i) {  // lane bits of each table index
+  for (int i = 1; i < sg.nst; ++i) {  // lane bits of each table index
     const DevStage st = cw.st[i];
     uint32_t b = 0;
     for (int w = 0; w < 2; ++w)
       if (st.u[w] < kLaneSrcEnd) b |= ((static_cast<uint32_t>(lane) >> st.u[w]) & 1u) << (1 + w);
-    cw.slane[i][lane] = static_cast<uint8_t>(b);
+    cw.slane[i - 1][lane] = static_cast<uint8_t>(b);
   }
   // the side-product tables depend on the tile only through tile-bit u's
   sc.ptab_tile = __any_sync(kFull, tile_dep);
