@@ -585,8 +585,10 @@ __device__ __forceinline__ void chain_term2(const ChainWarp& cw, const SegOpTab*
 // One paired tile (DevSeg::rb): chain_tile's walk with U = 1 for two Y rows
 // at once.  Row 1's stage-1 operands sit drow[t] further; everything else
 // (digit offsets, side products, climb control) is shared.  Each row sees
-// exactly the operation sequence of the unpaired walk.
-template <int NT, int NS, int K0>
+// exactly the operation sequence of the unpaired walk.  RM: bit t set if
+// stage-1 member t reads the row bit (drow[t] != 0); specialised for the
+// common masks, all members otherwise.
+template <int NT, int NS, int K0, int RM>
 __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                             const DevSeg& sg, V* __restrict__ arena,
                                             uint32_t tile, int lane) {
@@ -615,18 +617,29 @@ __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __res
     V v[2][2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
+      // [row][member] at s = 0 (m) and s = 1 (n); row 1 reloads only the
+      // members that read the row bit (RM), the others -- and the products
+      // of a row-invariant leading run -- are shared
+      V m[2][NT], n[2][NT];
+#pragma unroll
+      for (int t = K0 ? 1 : 0; t < NT; ++t) {
+        const uint32_t oq = o[t] + (q ? d0[t] : 0u);
+        m[0][t] = ld(B[t] + oq);
+        m[1][t] = ((RM >> t) & 1) ? ld(B[t] + oq + dr[t]) : m[0][t];
+        if (NS) {
+          n[0][t] = ld(B[t] + oq + sdl[t]);
+          n[1][t] = ((RM >> t) & 1) ? ld(B[t] + oq + sdl[t] + dr[t]) : n[0][t];
+        }
+      }
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        uint32_t oq[NT];
+        V x = K0 ? rscale(r0, m[r][1]) : m[r][0];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) oq[t] = o[t] + (q ? d0[t] : 0u) + (r ? dr[t] : 0u);
-        V x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
-#pragma unroll
-        for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
+        for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, m[r][t]);
         if (NS) {
-          V p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
+          V p = K0 ? rscale(r0, n[r][1]) : n[r][0];
 #pragma unroll
-          for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
+          for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, n[r][t]);
           x = cadd(x, p);
         }
         v[q][r] = x;
@@ -653,6 +666,16 @@ __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __res
       y[y1] = x1;
     }
   }
+}
+
+// chain_tile2 specialised for the row-bit member mask rm if it is one of RMs.
+template <int NT, int NS, int K0, int... RMs>
+__device__ __forceinline__ bool chain_tile2_masks(int rm, ChainWarp& cw,
+                                                  const SegOpTab* __restrict__ tab,
+                                                  const DevSeg& sg, V* __restrict__ arena,
+                                                  uint32_t tile, int lane) {
+  return ((rm == RMs ? (chain_tile2<NT, NS, K0, RMs>(cw, tab, sg, arena, tile, lane), true)
+                     : false) || ...);
 }
 
 // One tile: 2^J stage-1 evaluations (NT members, NS summed bits), in groups
@@ -831,8 +854,28 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
   }
   if constexpr (NT <= kSegPairMaxNt) {
     if (sg.rb != kNoVar) {  // paired rows
-      if (k0) chain_tile2<NT, NS, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
-      else chain_tile2<NT, NS, 0>(cw, tab, sg, arena, tile, lane);
+      constexpr int kAll = (1 << NT) - 1;
+      int rm = 0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) rm |= cw.drow[t] ? 1 << t : 0;
+      if (k0) {
+        constexpr int K = NT >= 2 ? 1 : 0;
+        if constexpr (NS == 1 && NT == 3) {
+          if (chain_tile2_masks<3, 1, K, 2, 4>(rm & ~1, cw, tab, sg, arena, tile, lane)) return;
+        }
+        if constexpr (NS == 1 && NT == 4) {
+          if (chain_tile2_masks<4, 1, K, 4, 8, 12>(rm & ~1, cw, tab, sg, arena, tile, lane)) return;
+        }
+        chain_tile2<NT, NS, K, kAll>(cw, tab, sg, arena, tile, lane);
+      } else {
+        if constexpr (NS == 1 && NT == 2) {
+          if (chain_tile2_masks<2, 1, 0, 1, 2>(rm, cw, tab, sg, arena, tile, lane)) return;
+        }
+        if constexpr (NS == 1 && NT == 3) {
+          if (chain_tile2_masks<3, 1, 0, 2, 4>(rm, cw, tab, sg, arena, tile, lane)) return;
+        }
+        chain_tile2<NT, NS, 0, kAll>(cw, tab, sg, arena, tile, lane);
+      }
       return;
     }
   }
