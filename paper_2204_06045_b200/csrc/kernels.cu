@@ -586,9 +586,10 @@ __device__ __forceinline__ void chain_term2(const ChainWarp& cw, const SegOpTab*
 // at once.  Row 1's stage-1 operands sit drow[t] further; everything else
 // (digit offsets, side products, climb control) is shared.  Each row sees
 // exactly the operation sequence of the unpaired walk.  RM: bit t set if
-// stage-1 member t reads the row bit (drow[t] != 0); specialised for the
-// common masks, all members otherwise.
-template <int NT, int NS, int K0, int RM>
+// stage-1 member t reads the row bit (drow[t] != 0); DM: bit t set if it
+// does not read digit bit 0 (dj[0] == 0).  Specialised for the common masks;
+// otherwise RM = all members, DM = none.
+template <int NT, int NS, int K0, int RM, int DM>
 __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                             const DevSeg& sg, V* __restrict__ arena,
                                             uint32_t tile, int lane) {
@@ -614,21 +615,38 @@ __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __res
 #pragma unroll
       for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t];
     }
+    // [row][member] at s = 0 (m) and s = 1 (n).  Row 1 reloads only the
+    // members that read the row bit (RM), q = 1 only those that read digit
+    // bit 0 (not in DM); the rest -- and the products of an invariant
+    // leading run -- are shared
+    V km[2][NT], kn[2][NT];  // q = 0 values of the DM members
     V v[2][2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      // [row][member] at s = 0 (m) and s = 1 (n); row 1 reloads only the
-      // members that read the row bit (RM), the others -- and the products
-      // of a row-invariant leading run -- are shared
       V m[2][NT], n[2][NT];
 #pragma unroll
       for (int t = K0 ? 1 : 0; t < NT; ++t) {
+        if (q == 1 && ((DM >> t) & 1)) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            m[r][t] = km[r][t];
+            n[r][t] = kn[r][t];
+          }
+          continue;
+        }
         const uint32_t oq = o[t] + (q ? d0[t] : 0u);
         m[0][t] = ld(B[t] + oq);
         m[1][t] = ((RM >> t) & 1) ? ld(B[t] + oq + dr[t]) : m[0][t];
         if (NS) {
           n[0][t] = ld(B[t] + oq + sdl[t]);
           n[1][t] = ((RM >> t) & 1) ? ld(B[t] + oq + sdl[t] + dr[t]) : n[0][t];
+        }
+        if (q == 0 && ((DM >> t) & 1)) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            km[r][t] = m[r][t];
+            kn[r][t] = n[r][t];
+          }
         }
       }
 #pragma unroll
@@ -668,14 +686,16 @@ __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __res
   }
 }
 
-// chain_tile2 specialised for the row-bit member mask rm if it is one of RMs.
-template <int NT, int NS, int K0, int... RMs>
-__device__ __forceinline__ bool chain_tile2_masks(int rm, ChainWarp& cw,
+// chain_tile2 specialised for the member masks key = RM | DM << 8 if it is
+// one of Keys.
+template <int NT, int NS, int K0, int... Keys>
+__device__ __forceinline__ bool chain_tile2_masks(int key, ChainWarp& cw,
                                                   const SegOpTab* __restrict__ tab,
                                                   const DevSeg& sg, V* __restrict__ arena,
                                                   uint32_t tile, int lane) {
-  return ((rm == RMs ? (chain_tile2<NT, NS, K0, RMs>(cw, tab, sg, arena, tile, lane), true)
-                     : false) || ...);
+  return ((key == Keys ? (chain_tile2<NT, NS, K0, (Keys & 0xff), (Keys >> 8)>(cw, tab, sg, arena,
+                                                                          tile, lane), true)
+                       : false) || ...);
 }
 
 // One tile: 2^J stage-1 evaluations (NT members, NS summed bits), in groups
@@ -855,26 +875,33 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
   if constexpr (NT <= kSegPairMaxNt) {
     if (sg.rb != kNoVar) {  // paired rows
       constexpr int kAll = (1 << NT) - 1;
-      int rm = 0;
+      int key = 0;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) rm |= cw.drow[t] ? 1 << t : 0;
+      for (int t = 0; t < NT; ++t)
+        key |= (cw.drow[t] ? 1 << t : 0) | (__ldg(&tab[t].dj[0]) ? 0 : 256 << t);
       if (k0) {
         constexpr int K = NT >= 2 ? 1 : 0;
+        key &= ~0x101;
         if constexpr (NS == 1 && NT == 3) {
-          if (chain_tile2_masks<3, 1, K, 2, 4>(rm & ~1, cw, tab, sg, arena, tile, lane)) return;
+          if (chain_tile2_masks<3, 1, K, 2, 4, 6 | 4 << 8>(key, cw, tab, sg, arena, tile, lane))
+            return;
         }
         if constexpr (NS == 1 && NT == 4) {
-          if (chain_tile2_masks<4, 1, K, 4, 8, 12>(rm & ~1, cw, tab, sg, arena, tile, lane)) return;
+          if (chain_tile2_masks<4, 1, K, 4, 8, 12, 12 | 2 << 8, 4 | 2 << 8, 8 | 2 << 8>(
+                  key, cw, tab, sg, arena, tile, lane))
+            return;
         }
-        chain_tile2<NT, NS, K, kAll>(cw, tab, sg, arena, tile, lane);
+        chain_tile2<NT, NS, K, kAll, 0>(cw, tab, sg, arena, tile, lane);
       } else {
         if constexpr (NS == 1 && NT == 2) {
-          if (chain_tile2_masks<2, 1, 0, 1, 2>(rm, cw, tab, sg, arena, tile, lane)) return;
+          if (chain_tile2_masks<2, 1, 0, 1, 2>(key, cw, tab, sg, arena, tile, lane)) return;
         }
         if constexpr (NS == 1 && NT == 3) {
-          if (chain_tile2_masks<3, 1, 0, 2, 4>(rm, cw, tab, sg, arena, tile, lane)) return;
+          if (chain_tile2_masks<3, 1, 0, 2, 4, 4 | 1 << 8, 2 | 1 << 8>(key, cw, tab, sg, arena,
+                                                                      tile, lane))
+            return;
         }
-        chain_tile2<NT, NS, 0, kAll>(cw, tab, sg, arena, tile, lane);
+        chain_tile2<NT, NS, 0, kAll, 0>(cw, tab, sg, arena, tile, lane);
       }
       return;
     }
