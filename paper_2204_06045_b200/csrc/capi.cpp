@@ -639,8 +639,11 @@ qtng_status qtng_plan_dump(int n, int m, const int* edges, int p, int merged,
       if (w.fail_code) throw Error(w.fail_code, w.fail_msg);
       ptrs.push_back(&w);
     }
-    // every op as its own device op (no chain fusion): the op-class view
-    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, false, true);
+    // every op as its own device op (no chain fusion): the op-class view;
+    // QTNG_DUMP_FUSED=1: the level ops of the fused program instead
+    const char* fz = std::getenv("QTNG_DUMP_FUSED");
+    const bool fuse = fz && fz[0] == '1';
+    const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse, true);
     std::vector<int> out;
     for (size_t L = 0; L < hp.levels.size(); ++L)
       for (uint32_t k = 0; k < hp.levels[L].op_count + hp.levels[L].outer_count; ++k) {

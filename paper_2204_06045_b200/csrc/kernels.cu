@@ -237,7 +237,12 @@ template <int MAXT>
 #ifndef QTNG_MINB_T4
 #define QTNG_MINB_T4 3
 #endif
-__global__ void __launch_bounds__(kThreads, MAXT <= 2 ? QTNG_MINB_T2 : (MAXT <= 4 ? QTNG_MINB_T4 : 2))
+#ifndef QTNG_MINB_T6
+#define QTNG_MINB_T6 4
+#endif
+__global__ void __launch_bounds__(kThreads, MAXT <= 2 ? QTNG_MINB_T2
+                                            : (MAXT <= 4 ? QTNG_MINB_T4
+                                                         : (MAXT <= 6 ? QTNG_MINB_T6 : 2)))
 level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
              const DevTensor* __restrict__ trefs, V* __restrict__ arena,
              uint32_t op_count, uint32_t items) {
@@ -1335,6 +1340,8 @@ cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
     level_kernel<2><<<grid_for<2>(lv.items), kThreads, 0, s>>>(o, b, trefs, arena, lv.op_count, lv.items);
   else if (lv.max_nt <= 4)
     level_kernel<4><<<grid_for<4>(lv.items), kThreads, 0, s>>>(o, b, trefs, arena, lv.op_count, lv.items);
+  else if (lv.max_nt <= 6)
+    level_kernel<6><<<grid_for<6>(lv.items), kThreads, 0, s>>>(o, b, trefs, arena, lv.op_count, lv.items);
   else
     level_kernel<8><<<grid_for<8>(lv.items), kThreads, 0, s>>>(o, b, trefs, arena, lv.op_count, lv.items);
   return cudaGetLastError();
