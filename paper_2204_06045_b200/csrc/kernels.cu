@@ -52,6 +52,9 @@ constexpr int kThreads = 256;
 constexpr int kWarpsPerCta = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSmemOps = 4096;  // item_begin entries cached in shared memory
+#ifndef QTNG_LEVEL_CACHE_MIN
+#define QTNG_LEVEL_CACHE_MIN 0u  // items per warp from which a CTA caches the item table (tuned)
+#endif
 
 __device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
@@ -251,10 +254,9 @@ level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
 #endif
   __shared__ DevTensor slots[kWarpsPerCta][MAXT];
   __shared__ uint32_t sbeg[kSmemOps];
-  // cache the item table in shared memory only when each warp will look it
-  // up several times (small levels: a couple of binary searches in L1/L2 are
-  // cheaper than every CTA copying the whole table)
-  const bool cached = op_count <= kSmemOps && items >= 4u * gridDim.x * kWarpsPerCta;
+  // cache the item table in shared memory (the cooperative copy costs one
+  // round trip; a binary search in global memory costs ~12 dependent ones)
+  const bool cached = op_count <= kSmemOps && items >= QTNG_LEVEL_CACHE_MIN * gridDim.x * kWarpsPerCta;
   if (cached)
     for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
   __syncthreads();
@@ -382,10 +384,9 @@ outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
 #endif
   __shared__ DevTensor slots[kWarpsPerCta][4];
   __shared__ uint32_t sbeg[kSmemOps];
-  // cache the item table in shared memory only when each warp will look it
-  // up several times (small levels: a couple of binary searches in L1/L2 are
-  // cheaper than every CTA copying the whole table)
-  const bool cached = op_count <= kSmemOps && items >= 4u * gridDim.x * kWarpsPerCta;
+  // cache the item table in shared memory (the cooperative copy costs one
+  // round trip; a binary search in global memory costs ~12 dependent ones)
+  const bool cached = op_count <= kSmemOps && items >= QTNG_LEVEL_CACHE_MIN * gridDim.x * kWarpsPerCta;
   if (cached)
     for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
   __syncthreads();
