@@ -5,12 +5,37 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 
 #include "pool.hpp"
 
 namespace qtng {
+
+namespace {
+// QTNG_TIMING=2: phase times of build_plan on stderr (host tuning aid)
+struct PlanTimer {
+  bool on;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  PlanTimer() {
+    static const bool e = [] {
+      const char* v = std::getenv("QTNG_TIMING");
+      return v && v[0] == '2';
+    }();
+    on = e;
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "build_plan %s %.3f ms\n", what,
+                 std::chrono::duration<double>(now - t).count() * 1e3);
+    t = now;
+  }
+};
+}  // namespace
+
 
 namespace {
 
@@ -151,6 +176,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     }
   auto op_at = [&](uint32_t g) -> const Op& { return cones[lc_of[g]]->ops[g - base[lc_of[g]]]; };
 
+  PlanTimer ptm;
   // ---- units: single ops, or fused chains (segments, see device_plan.hpp)
   // main_pos[g]: position of op g's fused main member, -1 when g heads its unit
   std::vector<int8_t> main_pos(N, -1);
@@ -203,6 +229,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   for (int c = 0; c < C; ++c) ubase[c + 1] = ubase[c] + static_cast<uint32_t>(cus[c].first.size());
   const uint32_t U = ubase[C];
   std::vector<uint32_t> unit_first(U), unit_last(U), unit_len(U), unit_nops(U);
+  ptm.mark("units");
   // unit levels: 1 + the deepest unit producing a materialised input; units
   // are visited in the order of their last op (producers come first)
   std::vector<int32_t> unit_level(U, 0);
@@ -267,6 +294,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     }
   }
 
+  ptm.mark("levels");
   // arena placement of unit outputs over level lifetimes; scalars / kept
   // results live to the end; fused intermediates get no storage
   constexpr uint64_t kNoOut = ~uint64_t{0};
@@ -303,6 +331,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   auto seg_cy = [&](uint32_t u) {
     return std::min<int>(op_at(unit_last[u]).r, level_cy[unit_level[u]]);
   };
+  ptm.mark("arena");
   // outer-join classification of single-op units (DevOp::lead/rb), in parallel
   std::vector<uint32_t> outer_sig(N, 0);  // 0 = generic; else 1 | lead<<8 | rb0<<16 | rb1<<24
   {
@@ -356,6 +385,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
                        return ga == 2 && seg_cost(a) > seg_cost(b);
                      });
 
+  ptm.mark("outer+order");
   // descriptors, level by level: item/tref prefix sums sequentially ...
   std::vector<uint32_t> unit_slot(U);   // index into hp.ops or hp.segs
   std::vector<uint32_t> unit_tref(U);
@@ -434,6 +464,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       hp.levels.push_back(ll);
     }
   }
+  ptm.mark("prefix");
   // ... then every operand's bit map in parallel chunks
   hp.trefs.resize(n_trefs);
   std::vector<double> op_bytes(N, 0.0), unit_dev_bytes(U, 0.0);
@@ -563,6 +594,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       unit_dev_bytes[u] = dev_bytes;
     }
   });
+  ptm.mark("fill");
   // segment work items (tiles; half as many for paired segments), per level
   for (LevelLaunch& ll : hp.levels) {
     ll.seg_items = 0;
@@ -651,6 +683,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     }
   }
 
+  ptm.mark("accounting");
   // records (one per non-empty bucket, walk order) and per-lightcone scalars
   hp.rec_begin.reserve(C + 1);
   hp.rec_begin.push_back(0);
@@ -671,6 +704,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     for (int s : w.scalars) hp.scalar_off.push_back(out[base[c] + s]);
     hp.lc_begin.push_back(static_cast<uint32_t>(hp.scalar_off.size()));
   }
+  ptm.mark("records");
   return hp;
 }
 
