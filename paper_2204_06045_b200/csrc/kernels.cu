@@ -1217,6 +1217,9 @@ int seg_grid(uint32_t items) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#ifdef QTNG_SEG_CARVEOUT  // tuning: preferred shared-memory carveout (percent)
+    cudaFuncSetAttribute(seg_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, QTNG_SEG_CARVEOUT);
+#endif
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_kernel, 32 * kSegWarps, 0);
     cap = sms * (per_sm > 0 ? per_sm : 1);
   }
