@@ -595,7 +595,32 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     }
   });
   ptm.mark("fill");
-  // segment work items (tiles; half as many for paired segments), per level
+  // segment work items (tiles; half as many for paired segments), per level;
+  // a paired tile costs about two, so re-sort each level's segments by tile
+  // cost (LPT order of the dynamic tile queue) and remap unit_slot
+  {
+    std::vector<uint32_t> perm, slot_of(hp.segs.size());
+    std::vector<DevSeg> tmp;
+    auto tile_cost = [&](const DevSeg& sg) {
+      return (uint64_t{1} << (sg.nst - 1)) * (sg.nops + hp.stages[sg.stage].nt) *
+             (sg.rb != kNoVar ? 2u : 1u);
+    };
+    for (const LevelLaunch& ll : hp.levels) {
+      perm.resize(ll.seg_count);
+      for (uint32_t k = 0; k < ll.seg_count; ++k) perm[k] = ll.seg_begin + k;
+      std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+        return tile_cost(hp.segs[a]) > tile_cost(hp.segs[b]);
+      });
+      tmp.resize(ll.seg_count);
+      for (uint32_t k = 0; k < ll.seg_count; ++k) {
+        tmp[k] = hp.segs[perm[k]];
+        slot_of[perm[k]] = ll.seg_begin + k;
+      }
+      std::copy(tmp.begin(), tmp.end(), hp.segs.begin() + ll.seg_begin);
+    }
+    for (uint32_t u = 0; u < U; ++u)
+      if (unit_len[u] > 1) unit_slot[u] = slot_of[unit_slot[u]];
+  }
   for (LevelLaunch& ll : hp.levels) {
     ll.seg_items = 0;
     for (uint32_t k = ll.seg_begin; k < ll.seg_begin + ll.seg_count; ++k) {
