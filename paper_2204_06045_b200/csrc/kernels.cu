@@ -707,7 +707,8 @@ __device__ __forceinline__ bool chain_tile2_masks(int key, ChainWarp& cw,
 // One tile: 2^J stage-1 evaluations (NT members, NS summed bits), in groups
 // of 2^U consecutive j (stages 2..U+1 resolved in registers, four independent
 // stage-1 products in flight), then the climb above each group.
-template <int NT, int NS, int U, int K0>
+// DM: bit t set if member t does not read digit bit 0 (loaded once per pair).
+template <int NT, int NS, int U, int K0, int DM = 0>
 __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                            const DevSeg& sg, V* __restrict__ arena,
                                            uint32_t tile, int lane) {
@@ -736,18 +737,32 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
       for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t] + d1[t];
     }
     V v[G];
+    V km[NT], kn[NT];  // even-q values of the DM members
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      uint32_t oq[NT];
+      V m[NT], n[NT];  // member values at s = 0 / s = 1
 #pragma unroll
-      for (int t = 0; t < NT; ++t) oq[t] = o[t] + ((q & 1) ? d0[t] : 0u) + ((q & 2) ? d1[t] : 0u);
-      V x = K0 ? rscale(r0, ld(B[1] + oq[1])) : ld(B[0] + oq[0]);
+      for (int t = K0 ? 1 : 0; t < NT; ++t) {
+        if ((q & 1) && ((DM >> t) & 1)) {
+          m[t] = km[t];
+          n[t] = kn[t];
+          continue;
+        }
+        const uint32_t oq = o[t] + ((q & 1) ? d0[t] : 0u) + ((q & 2) ? d1[t] : 0u);
+        m[t] = ld(B[t] + oq);
+        if (NS) n[t] = ld(B[t] + oq + sdl[t]);
+        if (!(q & 1) && ((DM >> t) & 1)) {
+          km[t] = m[t];
+          kn[t] = n[t];
+        }
+      }
+      V x = K0 ? rscale(r0, m[1]) : m[0];
 #pragma unroll
-      for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, ld(B[t] + oq[t]));
+      for (int t = K0 ? 2 : 1; t < NT; ++t) x = cmul(x, m[t]);
       if (NS) {
-        V p = K0 ? rscale(r0, ld(B[1] + oq[1] + sdl[1])) : ld(B[0] + oq[0] + sdl[0]);
+        V p = K0 ? rscale(r0, n[1]) : n[0];
 #pragma unroll
-        for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, ld(B[t] + oq[t] + sdl[t]));
+        for (int t = K0 ? 2 : 1; t < NT; ++t) p = cmul(p, n[t]);
         x = cadd(x, p);
       }
       v[q] = x;
@@ -917,6 +932,13 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
     if (k0) chain_tile<NT, NS, U, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
     else chain_tile<NT, NS, U, 0>(cw, tab, sg, arena, tile, lane);
     return;
+  }
+  if constexpr (NS == 1 && NT == 5) {  // the unpaired 5-member C2 head: members 1, 3 lack digit 0
+    if (k0 && !__ldg(&tab[1].dj[0]) && __ldg(&tab[2].dj[0]) && !__ldg(&tab[3].dj[0]) &&
+        __ldg(&tab[4].dj[0])) {
+      chain_tile<5, 1, 1, 1, 10>(cw, tab, sg, arena, tile, lane);
+      return;
+    }
   }
   if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
   else chain_tile<NT, NS, 1, 0>(cw, tab, sg, arena, tile, lane);
