@@ -18,8 +18,12 @@ e2e   : the public API end to end -- energy_expectation(graph, angles) with host
         wall-clock, max over ranks.  The one-shot call pipelines lightcone
         chunks over 3 stream lanes (chunk c+1 is planned on the host while
         chunks <= c run), so host planning overlaps device work.
-Multi-GPU: edges LPT-sharded by predicted bytes, one NCCL reduce of the terms
-(total work fixed as N grows: "strong" scaling).
+Multi-GPU: edges LPT-sharded by predicted work (the library's qtng_shard_edges,
+the placement its single-process driver qtng_energy_multi uses too), one NCCL
+reduce of the terms (total work fixed as N grows: "strong" scaling).
+Sub-records (N=1, rank 0): `c4` (N=100 p=3, the 8-GPU config, on one GPU:
+value, e2e, parity), `c64` (C2 in the complex64 mode: value, error), and
+`multi_api` (qtng_energy_multi on this one device: the C-ABI multi-GPU path).
 --impl reference: the reference's own energy_expectation (oracle/_ref, built
 from /root/reference unmodified), matmul backend, jobs = all host threads.
 """
@@ -78,6 +82,15 @@ def fp64_pipe_peak(dev_index, sm_max_mhz, lanes=64):
     import torch
     sms = torch.cuda.get_device_properties(dev_index).multi_processor_count
     return sms * lanes * (sm_max_mhz or 1965.0) * 1e6, sms
+
+
+def measured_fp64_peak(q, dev_index):
+    """The FP64 rates measured on this GPU right now by the library's own
+    microkernels (qtng_fp64_peak, csrc/peak.cu): DMUL+DADD op/s, DFMA flop/s."""
+    try:
+        return q.fp64_peak(dev_index)
+    except Exception:
+        return None, None
 
 
 def golden_energy(name):
@@ -262,8 +275,7 @@ def run_b200(args, cfg):
     g = q.random_regular(cfg["n"], cfg["d"], cfg["seed"])
     a = q.Angles(cfg["gammas"], cfg["betas"])
     p = a.depth()
-    costs = q.edge_costs(g, p)
-    shards = qd.lpt_shard(costs, world)
+    shards = qd.shards_for(q, g, p, world)
     mine = shards[rank]
     ecfg = q.EngineConfig(dtype=args.dtype)
     plan = q.Plan(g, p, edges=mine, ctx=ctx, cfg=ecfg)
@@ -332,6 +344,13 @@ def run_b200(args, cfg):
     # BASELINE configs[2]: the calibration bucket [w,2]->w-1 (engine.cpp:371-390)
     # as one level_kernel op, HBM-bound, timed alone (rank 0 only)
     c3 = microbench_c3(ctx) if rank == 0 and not args.no_c3 else None
+    subs = {}
+    if world == 1 and not args.no_sub:
+        subs["c4"] = sub_c4(q, ctx, args)
+        if args.dtype == "c128":
+            subs["c64"] = sub_c64(q, ctx, cfg, args)
+        subs["multi_api"] = sub_multi(q, ctx, cfg, args)
+    mpk_ma, mpk_fma = measured_fp64_peak(q, local)
 
     if rank != 0:
         return 0
@@ -341,9 +360,16 @@ def run_b200(args, cfg):
     gold = golden_energy(args.config)
     csum = clocks.summary()
     c64 = args.dtype == "c64"
-    fp_peak, sms = fp64_pipe_peak(local, csum.get("sm_max_mhz"), 128 if c64 else 64)
-    seg_s = kms["seg_kernel"] / 1e3
-    lvl_s = kms["level_kernel"] / 1e3
+    fp_peak_derived, sms = fp64_pipe_peak(local, csum.get("sm_max_mhz"), 128 if c64 else 64)
+    fp_peak = mpk_ma if (mpk_ma and not c64) else fp_peak_derived
+    # per-kernel device time INSIDE the measured graph replay: the step time
+    # apportioned by the kernels' shares of the eager run's per-kernel CUDA
+    # events (the kernels of one level overlap, so these shares sum the
+    # kernels' own durations; the result never exceeds ms_per_step)
+    ksum = max(1e-9, sum(kms.values()))
+    kshare = {k: v / ksum for k, v in kms.items()}
+    seg_s = ms_per_step * kshare["seg_kernel"] / 1e3
+    lvl_s = ms_per_step * kshare["level_kernel"] / 1e3
     seg_ach = info.seg_fp64_ops / seg_s / 1e12 if seg_s > 0 else None
     lvl_ach = info.single_alg_bytes / lvl_s / 1e9 if lvl_s > 0 else None
     out = {
@@ -376,27 +402,37 @@ def run_b200(args, cfg):
                      "achieved": seg_ach, "peak": fp_peak / 1e12, "unit": "TFLOP/s",
                      "frac": (seg_ach * 1e12 / fp_peak) if seg_ach else None,
                      "peak_source": (f"derived: {sms} SMs x 128 FP32 lanes x sm_max_mhz" if c64 else
-                                     f"derived: {sms} SMs x 64 FP64 lanes x sm_max_mhz "
-                                     "(DMUL/DADD issue rate; NVIDIA's FP64 figure counts DFMA as 2)"),
+                                     ("measured in this run: qtng_fp64_peak (csrc/peak.cu), "
+                                      "DMUL+DADD ops/s over 8 independent chains per thread"
+                                      if mpk_ma else
+                                      f"derived: {sms} SMs x 64 FP64 lanes x sm_max_mhz")),
+                     "peak_derived": fp_peak_derived / 1e12,
+                     "peak_fma_tflops_measured": (mpk_fma / 1e12) if mpk_fma else None,
                      **committed_traffic("seg_kernel"),
                      "flops_per_step": info.seg_fp64_ops,
                      "flops_def": "the reference NaiveBackend loop's FP64 mul+add count of the "
                                   "buckets seg_kernel evaluates",
-                     "kernel_ms_per_step": kms["seg_kernel"],
-                     "share_of_kernel_time": kms["seg_kernel"] / max(1e-9, sum(kms.values()))},
+                     "kernel_ms_per_step": ms_per_step * kshare["seg_kernel"],
+                     "kernel_ms_def": "ms_per_step (graph replay) x seg_kernel's share of the "
+                                      "per-kernel event times of an eager run",
+                     "eager_kernel_ms": kms,
+                     "share_of_kernel_time": kshare["seg_kernel"]},
         "roofline_level_kernel": {"bound": "hbm", "kernel": "level_kernel (unfused buckets)",
                                   "achieved": lvl_ach, "peak": peak, "unit": "GB/s",
                                   "frac": (lvl_ach / peak) if lvl_ach else None,
                                   "peak_source": peak_kind,
                                   **committed_traffic("level_kernel"),
                                   "alg_bytes_per_step": info.single_alg_bytes,
-                                  "kernel_ms_per_step": kms["level_kernel"]},
+                                  "kernel_ms_per_step": ms_per_step * kshare["level_kernel"]},
         "roofline_step": {"alg_bytes_per_step": info.alg_bytes,
                           "dev_bytes_per_step": info.dev_bytes,
                           "fp64_ops_per_step": info.fp64_ops,
                           "effective_GBps": info.alg_bytes / (ms_per_step / 1e3) / 1e9,
                           "unfused_hbm_roofline_ms": info.alg_bytes / (peak * 1e9) * 1e3,
                           "fp64_roofline_ms": info.fp64_ops / fp_peak * 1e3,
+                          "fused_hbm_floor_ms": info.dev_bytes / (peak * 1e9) * 1e3,
+                          "fused_floors_note": "the fused program's own floors: dev_bytes at "
+                                               "measured HBM, fp64_ops at the FP64 peak above",
                           "level_events_ms": lvl_kernel_ms,
                           "note": "alg_bytes = the reference's per-bucket accounting "
                                   "(SURVEY 8a); dev_bytes = what the fused program must move"},
@@ -412,12 +448,97 @@ def run_b200(args, cfg):
         "arena_bytes": int(info.arena_bytes),
         "segments": int(info.n_segments), "fused_buckets": int(info.n_fused_ops),
     }
+    out.update(subs)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _golden_config(name):
+    with open(os.path.join(ROOT, "tests", "golden", "energies.json")) as f:
+        return json.load(f)["configs"][name]
+
+
+def sub_c4(q, ctx, args, steps=10):
+    """BASELINE configs[3] (N=100 p=3, the 8-GPU config) on this one GPU:
+    device-resident value (graph replay), e2e through energy_expectation,
+    parity against the reference's naive energy, and the LPT shard balance
+    the 8-way run would see (predicted work)."""
+    import numpy as np
+    import torch
+    from paper_2204_06045_b200 import dist as qd
+    cfg = CONFIGS["C4"]
+    g = q.random_regular(cfg["n"], 3, cfg["seed"])
+    a = q.Angles(cfg["gammas"], cfg["betas"])
+    plan = q.Plan(g, 3, ctx=ctx)
+    terms = plan.execute(a)
+    plan.run_device(3)
+    dev_ms = plan.run_device(steps) / steps
+    replay_terms = plan.terms()
+    e = 0.5 * g.m
+    for x in replay_terms.real:
+        e -= 0.5 * float(x)
+    for _ in range(2):
+        q.energy_expectation(g, a, q.GpuBackend(ctx))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = q.energy_expectation(g, a, q.GpuBackend(ctx))
+    e2e_ms = 1e3 * (time.perf_counter() - t0) / steps
+    gold = _golden_config("C4")
+    work = q.edge_work(g, 3)
+    shards = qd.shards_for(q, g, 3, 8)
+    loads = [float(sum(work[i] for i in s)) for s in shards]
+    info = plan.info()
+    plan.close()
+    return {"workload": cfg["workload"], "value": g.m / (dev_ms / 1e3), "unit": "lightcones/s",
+            "ms_per_step": dev_ms, "e2e": {"value": g.m / (e2e_ms / 1e3), "ms_per_step": e2e_ms},
+            "energy": res.energy, "energy_golden_naive": gold["energy_naive"],
+            "parity_bit_exact": res.energy == gold["energy_naive"] and
+            bool(np.array_equal(replay_terms, terms)) and e == res.energy,
+            "levels": int(info.n_levels), "buckets": int(info.n_buckets),
+            "lpt8_predicted_speedup": float(sum(loads) / max(loads)),
+            "note": "seed 1 (the golden config); its largest lightcone caps 8-way lightcone "
+                    "sharding (SURVEY 8e)"}
+
+
+def sub_c64(q, ctx, cfg, args, steps=10):
+    """The complex64 mode (north_star: 1e-5) on the headline C2 workload."""
+    g = q.random_regular(cfg["n"], cfg["d"], cfg["seed"])
+    a = q.Angles(cfg["gammas"], cfg["betas"])
+    plan = q.Plan(g, a.depth(), ctx=ctx, cfg=q.EngineConfig(dtype="c64"))
+    plan.execute(a)
+    plan.run_device(3)
+    dev_ms = plan.run_device(steps) / steps
+    t = plan.terms()
+    e = 0.5 * g.m
+    for x in t.real:
+        e -= 0.5 * float(x)
+    gold = golden_energy("C2")
+    plan.close()
+    return {"value": g.m / (dev_ms / 1e3), "unit": "lightcones/s", "ms_per_step": dev_ms,
+            "dtype": "c64", "energy": e, "rel_err_vs_c128_golden": abs(e - gold) / abs(gold),
+            "tolerance": 1e-5}
+
+
+def sub_multi(q, ctx, cfg, args, steps=5):
+    """qtng_energy_multi (the single-process multi-GPU C driver: LPT shards,
+    one host thread per device, one ncclReduce) on the one device here."""
+    g = q.random_regular(cfg["n"], cfg["d"], cfg["seed"])
+    a = q.Angles(cfg["gammas"], cfg["betas"])
+    try:
+        res, ms = q.energy_multi(g, a, [ctx])
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res, ms = q.energy_multi(g, a, [ctx])
+        wall = 1e3 * (time.perf_counter() - t0) / steps
+    except Exception as ex:  # reported, not fatal
+        return {"error": repr(ex)}
+    return {"devices": 1, "e2e_ms_per_step": wall, "shard_ms": [float(x) for x in ms],
+            "energy": res.energy, "parity_bit_exact": res.energy == golden_energy("C2")}
 
 
 def microbench_c3(ctx, widths=(26, 28)):
@@ -479,6 +600,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the single-bucket microbench")
+    ap.add_argument("--no-sub", action="store_true", help="skip the C4 / c64 / multi sub-records")
     ap.add_argument("--dtype", choices=["c128", "c64"], default="c128",
                     help="c64: the optional complex64 mode (1e-5), not the headline")
     args = ap.parse_args()

@@ -85,13 +85,31 @@ typedef struct qtng_plan_info {
   double single_alg_bytes;   /* B_alg of the buckets run by level/outer kernels */
 } qtng_plan_info;
 
+/* The report of a one-shot energy: ContractionReport's aggregate fields as
+ * energy_expectation fills them (proj/include/qtnsim/engine.hpp:82-88,136-139;
+ * engine.cpp:548-556).  `records`/`rec_cap` are inputs (records may be NULL);
+ * one TimingRecord per contracted bucket, selection order, edge_u/edge_v set.
+ * elapsed_s is the bucket's share (by algorithmic bytes) of its program's
+ * measured device time: the level-batched kernels run hundreds of buckets at
+ * once, so a per-bucket device time does not exist. */
+typedef struct qtng_energy_report {
+  qtng_record* records;       /* in: caller buffer (may be NULL) */
+  int64_t rec_cap;            /* in: its capacity in records */
+  int64_t n_records;          /* out: records of the contracted buckets */
+  uint64_t peak_tensor_bytes; /* out: max over lightcones of 16 * 2^(largest result rank) */
+  int32_t merges_applied;     /* out: summed over lightcones (merge_buckets) */
+  int32_t merges_skipped;
+  float device_ms;            /* out: device time of the program(s) */
+} qtng_energy_report;
+
 /* ---------------------------------------------------------------- context */
 
 /* Create a context on CUDA `device`.  arena_bytes = initial HBM reservation
  * (0 = grow on demand). */
 qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out);
 void qtng_destroy(qtng_ctx* ctx);
-/* Arithmetic of the QAOA plans and energies created on ctx from now on:
+/* Default arithmetic of the QAOA plans and energies created on ctx with
+ * precision 0 (calls that pass 128 or 64 choose it themselves):
  * 128 (default) = complex128, bit-identical to the reference's naive backend;
  * 64 = complex64 arena and kernels (the north_star's optional mode, results
  * within 1e-5; complex128 per-lightcone products).  Explicit schedules and
@@ -116,11 +134,13 @@ qtng_status qtng_random_regular(int n, int d, uint64_t seed, int* edges, int cap
  * sorted edge list, flattened as: per bucket n_sum, sum_vars, n_tensors,
  * per tensor rank, vars; data = every tensor's entries (re, im) in the same
  * order (the format of oracle/qtn_oracle.h).  *n_ints / *n_data receive the
- * required sizes; nothing is written when a capacity is too small. */
+ * required sizes; nothing is written when a capacity is too small.  merges
+ * (may be NULL): the schedule's merges_applied, merges_skipped (ordering.hpp,
+ * counted like merge_buckets, engine.cpp:306-358; 0, 0 unmerged). */
 qtng_status qtng_edge_schedule(int n, int m, const int* edges, int p, const double* gammas,
                                const double* betas, int edge_index, int merged, int* ints,
                                int64_t int_cap, double* data, int64_t data_cap,
-                               int64_t* n_ints, int64_t* n_data, int* n_buckets);
+                               int64_t* n_ints, int64_t* n_data, int* n_buckets, int* merges);
 
 /* simulate_widths (proj/src/engine.cpp:235-240) of one edge's schedule. */
 qtng_status qtng_simulate_widths(int n, int m, const int* edges, int p, int edge_index,
@@ -178,21 +198,42 @@ qtng_status qtng_contract_schedule(qtng_ctx* ctx, int n_buckets, const int* ints
 
 /* energy_expectation (proj/src/engine.cpp:503-563): <C> = m/2 - 1/2 sum Re e_jk,
  * all lightcones of the selected edges on this device in one level-batched
- * program.  sel = NULL selects every edge; terms (may be NULL) receives
- * 2*n_sel doubles (e_jk re, im) in selection order.  The energy is only
- * meaningful when every edge is selected (it is m/2 - 1/2 sum over the
- * selection otherwise). */
+ * program.  precision: 0 (context default), 128 or 64.  sel = NULL selects
+ * every edge; terms (may be NULL) receives 2*n_sel doubles (e_jk re, im) in
+ * selection order.  *energy is NaN unless the selection is every edge in
+ * edge order (a partial selection has terms, not an energy).  report (may be
+ * NULL): peak bytes, merge counts, records. */
 qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
                         const double* gammas, const double* betas, int merged,
-                        int max_result_width, int n_sel, const int* sel, double* energy,
-                        double* terms);
+                        int max_result_width, int precision, int n_sel, const int* sel,
+                        double* energy, double* terms, qtng_energy_report* report);
+
+/* energy_expectation over several GPUs of one node: the edge pool of
+ * engine.cpp:531-541 becomes the devices.  The lightcones are placed by LPT
+ * on the predicted work (qtng_edge_work; qtng_shard_edges shows the
+ * placement), one host thread per context plans and contracts its shard
+ * (pipelined like qtng_energy), the final kernel writes each term into a
+ * 2m-double device vector (zero elsewhere), and ONE ncclReduce (sum, fp64)
+ * brings the vectors to ctxs[0]'s device.  The energy is summed there in edge
+ * order (engine.cpp:549-551), so it is bit-identical to the 1-GPU energy.
+ * Contexts must be on distinct devices.  terms (may be NULL): 2m doubles,
+ * edge order.  shard_ms (may be NULL): n_ctx device times. */
+qtng_status qtng_energy_multi(qtng_ctx* const* ctxs, int n_ctx, int n, int m, const int* edges,
+                              int p, const double* gammas, const double* betas, int merged,
+                              int max_result_width, int precision, double* energy, double* terms,
+                              float* shard_ms);
+/* Host-only: the shard (0..n_shards-1) qtng_energy_multi places each edge's
+ * lightcone on.  owner: m ints. */
+qtng_status qtng_shard_edges(int n, int m, const int* edges, int p, int merged, int n_shards,
+                             int* owner);
 
 /* ---------------------------------------------------------------- plans */
 
 /* Angle-independent plan of the selected edges' lightcones, uploaded to the
- * device once; executions then take only the 2p angles. */
+ * device once; executions then take only the 2p angles.  precision: 0
+ * (context default), 128 or 64. */
 qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int p, int merged,
-                             int max_result_width, int n_sel, const int* sel,
+                             int max_result_width, int precision, int n_sel, const int* sel,
                              qtng_plan** out);
 /* Device-resident plan of ONE explicit schedule (format of qtng_edge_schedule),
  * e.g. a single wide bucket for the C3 microbenchmark.  Its initial tensor
@@ -209,8 +250,17 @@ qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* i
 qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const double* betas,
                               double* terms, float* device_ms);
 /* Device-only re-execution with the current angles (no host copies), for
- * throughput measurement; n_runs back-to-back runs, total device time. */
+ * throughput measurement: the plan captured once as a CUDA graph, n_runs
+ * back-to-back replays, total device time. */
 qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms);
+/* FP64 pipe rates of `device` at its current clocks (peak.cu): DMUL+DADD
+ * operations per second (the instruction mix of the bucket kernels, which
+ * round every product and never fuse) and DFMA flops per second (2 per FMA).
+ * The roofline denominator of seg_kernel; MEASURED_PEAKS.json has no FP64 figure. */
+qtng_status qtng_fp64_peak(int device, double* mul_add_ops_per_s, double* fma_flops_per_s);
+/* The terms (2*n_sel doubles) the plan's last run left on the device --
+ * qtng_plan_execute or a qtng_plan_run_device graph replay. */
+qtng_status qtng_plan_terms(qtng_plan* plan, double* terms);
 qtng_status qtng_plan_info_get(const qtng_plan* plan, qtng_plan_info* info);
 /* State-vector oracle on the device: run_ansatz + expectation_cost
  * (proj/src/statevector.cpp:55-90) for n <= cap qubits (the reference's

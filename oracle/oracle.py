@@ -146,6 +146,8 @@ def ref_lib():
                                           C.POINTER(C.c_long), C.POINTER(C.c_int)]
         lib.ref_simulate_widths.argtypes = [C.c_int, C.c_int, _i32p, C.c_int, _f64p, _f64p,
                                             C.c_int, C.c_int, _i32p, C.c_int]
+        lib.ref_merge_counts.argtypes = [C.c_int, C.c_int, _i32p, C.c_int, _f64p, _f64p, C.c_int,
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]
         lib.ref_contract_bucket.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _i32p, _f64p,
                                             C.c_int, _i32p, _i32p, _f64p, C.c_long]
         lib.ref_contract_bucket_capped.argtypes = [C.c_int, _i32p, _i32p, C.c_int, _i32p,
@@ -245,6 +247,19 @@ def ref_edge_schedule(n, edges, gammas, betas, edge_index, merged=False):
             cap = int(-r) + 16
             continue
         return ints[:r].copy(), data[: dlen.value].copy(), nb.value
+
+
+def ref_merge_counts(n, edges, gammas, betas, edge_index):
+    """(merges_applied, merges_skipped) of one edge's merged schedule."""
+    lib = ref_lib()
+    e, m = _g(edges)
+    ap, sk = C.c_int(0), C.c_int(0)
+    st = lib.ref_merge_counts(n, m, e, len(gammas), np.asarray(gammas, np.float64),
+                              np.asarray(betas, np.float64), edge_index, C.byref(ap),
+                              C.byref(sk))
+    if st != 0:
+        _ref_err(st)
+    return ap.value, sk.value
 
 
 def ref_simulate_widths(n, edges, gammas, betas, edge_index, merged=False):

@@ -235,6 +235,21 @@ long ref_edge_schedule(int n, int m, const int* edges, int p, const double* gamm
   }
 }
 
+// merge_buckets' counters of one edge's merged schedule (engine.cpp:306-358).
+int ref_merge_counts(int n, int m, const int* edges, int p, const double* gammas,
+                     const double* betas, int edge_index, int* applied, int* skipped) {
+  try {
+    const Graph g = graph_from(n, m, edges);
+    const Angles a = angles_from(p, gammas, betas);
+    const ContractionSchedule s = edge_schedule(g, g.edges.at(edge_index), a, true);
+    *applied = s.merges_applied;
+    *skipped = s.merges_skipped;
+    return 0;
+  } catch (const std::exception& ex) {
+    return fail(ex);
+  }
+}
+
 // simulate_widths for one edge (engine.cpp:235-240).
 int ref_simulate_widths(int n, int m, const int* edges, int p, const double* gammas,
                         const double* betas, int edge_index, int merged, int* widths,

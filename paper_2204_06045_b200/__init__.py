@@ -11,7 +11,6 @@ CUDA for sm_100a).  There is no CPU fallback.
 """
 from __future__ import annotations
 
-import contextlib
 import ctypes as C
 import os
 import threading
@@ -20,7 +19,7 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._native import PlanInfo, Record, lib
+from ._native import EnergyReport, PlanInfo, Record, lib
 
 __all__ = [
     "InvalidInputError", "GenerationError", "ResourceError", "ScheduleError", "NumericalError",
@@ -273,15 +272,22 @@ def read_timing_csv(f) -> List["TimingRecord"]:
 
 @dataclass
 class ContractionReport:
+    """ContractionReport (engine.hpp:82-88)."""
+
     scalar: complex
     records: List[TimingRecord]
     peak_tensor_bytes: int
+    merges_applied: int = 0
+    merges_skipped: int = 0
 
 
 @dataclass
 class EnergyResult:
+    """EnergyResult (engine.hpp:136-139) plus the per-edge terms."""
+
     energy: float
     terms: np.ndarray  # complex e_jk per edge (edge order)
+    report: Optional[ContractionReport] = None
 
 
 # ------------------------------------------------------------------ context
@@ -293,17 +299,6 @@ class Context:
         _check(lib.qtng_create(device, arena_bytes, C.byref(h)))
         self._h = h
         self.device = device
-        self._prec_lock = threading.Lock()
-
-    @contextlib.contextmanager
-    def precision(self, bits: int):
-        """Plans and energies created inside use complex`bits` (128 or 64)."""
-        with self._prec_lock:
-            _check(lib.qtng_set_precision(self.handle, int(bits)))
-            try:
-                yield self
-            finally:
-                _check(lib.qtng_set_precision(self.handle, 128))
 
     @property
     def handle(self):
@@ -390,15 +385,19 @@ def edge_schedule(g: Graph, edge_index: int, angles: Angles,
     n_ints, n_data, nb = C.c_int64(0), C.c_int64(0), C.c_int(0)
     probe_i = np.zeros(1, np.int32)
     probe_d = np.zeros(1, np.float64)
+    merges = np.zeros(2, np.int32)
     _check(lib.qtng_edge_schedule(g.n, g.m, g.flat(), angles.depth(), gam, bet, edge_index,
                                   int(merged), probe_i, 0, probe_d, 0, C.byref(n_ints),
-                                  C.byref(n_data), C.byref(nb)))
+                                  C.byref(n_data), C.byref(nb), None))
     ints = np.zeros(max(1, n_ints.value), np.int32)
     data = np.zeros(max(1, n_data.value), np.float64)
     _check(lib.qtng_edge_schedule(g.n, g.m, g.flat(), angles.depth(), gam, bet, edge_index,
                                   int(merged), ints, len(ints), data, len(data),
-                                  C.byref(n_ints), C.byref(n_data), C.byref(nb)))
-    return _parse_flat(ints[: n_ints.value], data[: n_data.value], nb.value)
+                                  C.byref(n_ints), C.byref(n_data), C.byref(nb),
+                                  merges.ctypes.data_as(C.c_void_p)))
+    s = _parse_flat(ints[: n_ints.value], data[: n_data.value], nb.value)
+    s.merges_applied, s.merges_skipped = int(merges[0]), int(merges[1])
+    return s
 
 
 def _parse_flat(ints, data, n_buckets) -> ContractionSchedule:
@@ -562,9 +561,12 @@ def contract_network(schedule: ContractionSchedule, backend: Optional[GpuBackend
 
 def energy_expectation(g: Graph, angles: Angles, backend: Optional[GpuBackend] = None,
                        merged: bool = False, cfg: Optional[EngineConfig] = None,
-                       edges: Optional[Sequence[int]] = None) -> EnergyResult:
+                       edges: Optional[Sequence[int]] = None,
+                       records: bool = False) -> EnergyResult:
     """energy_expectation (engine.cpp:503-563): <C> = |E|/2 - 1/2 sum_e Re e_jk,
-    every lightcone contracted on the device in one level-batched program."""
+    every lightcone contracted on the device in one level-batched program.
+    With `edges` (a subset) the energy is NaN and the terms are the result.
+    records=True also returns the TimingRecords in result.report."""
     angles.validate()
     ctx = backend.ctx if backend is not None else default_context()
     cfg = cfg or EngineConfig()
@@ -573,12 +575,65 @@ def energy_expectation(g: Graph, angles: Angles, backend: Optional[GpuBackend] =
     k = g.m if sel is None else len(sel)
     terms = np.zeros(2 * max(1, k), np.float64)
     e = C.c_double(0)
-    with ctx.precision(cfg.precision_bits()):
+    rep = EnergyReport()
+    recs = None
+    if records:
+        # generous bound on the bucket count (the reference's lightcones hold
+        # < 300 buckets at the benchmark sizes); re-run with the exact count
+        # if it was not enough
+        cap = 512 * max(1, k)
+        recs = (Record * cap)()
+        rep.records, rep.rec_cap = C.cast(recs, C.c_void_p), cap
+    _check(lib.qtng_energy(ctx.handle, g.n, g.m, g.flat(), angles.depth(), gam, bet,
+                           int(merged), cfg.max_result_width, cfg.precision_bits(), k,
+                           None if sel is None else sel.ctypes.data_as(C.c_void_p),
+                           C.byref(e), terms, C.byref(rep)))
+    if records and rep.n_records > rep.rec_cap:
+        recs = (Record * rep.n_records)()
+        rep.records, rep.rec_cap = C.cast(recs, C.c_void_p), rep.n_records
         _check(lib.qtng_energy(ctx.handle, g.n, g.m, g.flat(), angles.depth(), gam, bet,
-                               int(merged), cfg.max_result_width, k,
+                               int(merged), cfg.max_result_width, cfg.precision_bits(), k,
                                None if sel is None else sel.ctypes.data_as(C.c_void_p),
-                               C.byref(e), terms))
-    return EnergyResult(e.value, terms[: 2 * k].view(np.complex128).copy())
+                               C.byref(e), terms, C.byref(rep)))
+    report = ContractionReport(
+        complex(e.value, 0.0),
+        [TimingRecord(r.edge_u, r.edge_v, r.bucket_seq, r.width, "b200", r.elapsed_s, r.ops,
+                      r.flops_est) for r in recs[: rep.n_records]] if records else [],
+        rep.peak_tensor_bytes, rep.merges_applied, rep.merges_skipped)
+    return EnergyResult(e.value, terms[: 2 * k].view(np.complex128).copy(), report)
+
+
+def fp64_peak(device: int = 0):
+    """Measured FP64 rates of `device` (qtng_fp64_peak): (DMUL+DADD ops/s, DFMA flops/s)."""
+    ma, fma = C.c_double(0), C.c_double(0)
+    _check(lib.qtng_fp64_peak(int(device), C.byref(ma), C.byref(fma)))
+    return ma.value, fma.value
+
+
+def shard_edges(g: Graph, p: int, n_shards: int, merged: bool = False) -> np.ndarray:
+    """The device (0..n_shards-1) energy_multi places each edge's lightcone on
+    (LPT on the predicted work, host-only)."""
+    out = np.zeros(max(1, g.m), np.int32)
+    _check(lib.qtng_shard_edges(g.n, g.m, g.flat(), p, int(merged), int(n_shards), out))
+    return out[: g.m]
+
+
+def energy_multi(g: Graph, angles: Angles, contexts: Sequence[Context], merged: bool = False,
+                 cfg: Optional[EngineConfig] = None):
+    """energy_expectation over several GPUs from ONE process (qtng_energy_multi):
+    LPT shards, one host thread per device, one ncclReduce of the term vector.
+    Returns (EnergyResult, per-device shard ms)."""
+    angles.validate()
+    cfg = cfg or EngineConfig()
+    gam, bet = _angles_arrays(angles)
+    hs = (C.c_void_p * len(contexts))(*[c.handle.value for c in contexts])
+    terms = np.zeros(2 * max(1, g.m), np.float64)
+    ms = np.zeros(max(1, len(contexts)), np.float32)
+    e = C.c_double(0)
+    _check(lib.qtng_energy_multi(hs, len(contexts), g.n, g.m, g.flat(), angles.depth(), gam,
+                                 bet, int(merged), cfg.max_result_width, cfg.precision_bits(),
+                                 C.byref(e), terms, ms))
+    return EnergyResult(e.value, terms[: 2 * g.m].view(np.complex128).copy()), ms[: len(contexts)]
 
 
 # ------------------------------------------------------------------ plans
@@ -598,10 +653,9 @@ class Plan:
         self.sel = (np.arange(g.m, dtype=np.int32) if edges is None
                     else np.ascontiguousarray(edges, dtype=np.int32))
         h = C.c_void_p()
-        with self.ctx.precision(cfg.precision_bits()):
-            _check(lib.qtng_plan_create(self.ctx.handle, g.n, g.m, g.flat(), p, int(merged),
-                                        cfg.max_result_width, len(self.sel),
-                                        self.sel.ctypes.data_as(C.c_void_p), C.byref(h)))
+        _check(lib.qtng_plan_create(self.ctx.handle, g.n, g.m, g.flat(), p, int(merged),
+                                    cfg.max_result_width, cfg.precision_bits(), len(self.sel),
+                                    self.sel.ctypes.data_as(C.c_void_p), C.byref(h)))
         self._h = h
         self.last_device_ms = 0.0
 
@@ -645,9 +699,17 @@ class Plan:
         return out[: 2 * len(self.sel)].view(np.complex128).copy()
 
     def run_device(self, n_runs: int = 1) -> float:
+        """n_runs replays of the plan's captured CUDA graph (current angles);
+        total device ms."""
         ms = C.c_float(0)
         _check(lib.qtng_plan_run_device(self._h, n_runs, C.byref(ms)))
         return ms.value
+
+    def terms(self) -> np.ndarray:
+        """The terms the last run (execute or a run_device replay) left on the device."""
+        out = np.zeros(2 * max(1, len(self.sel)), np.float64)
+        _check(lib.qtng_plan_terms(self._h, out))
+        return out[: 2 * len(self.sel)].view(np.complex128).copy()
 
     def level_ms(self) -> np.ndarray:
         n = self.info().n_levels

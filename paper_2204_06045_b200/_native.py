@@ -39,6 +39,14 @@ class PlanInfo(C.Structure):
                 ("single_alg_bytes", C.c_double)]
 
 
+class EnergyReport(C.Structure):
+    """qtng_energy_report: ContractionReport's aggregate fields (engine.hpp:82-88)."""
+
+    _fields_ = [("records", C.c_void_p), ("rec_cap", C.c_int64), ("n_records", C.c_int64),
+                ("peak_tensor_bytes", C.c_uint64), ("merges_applied", C.c_int32),
+                ("merges_skipped", C.c_int32), ("device_ms", C.c_float)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"native library {LIB_PATH} is missing; build it first "
@@ -56,7 +64,7 @@ def _load():
     lib.qtng_edge_schedule.argtypes = [C.c_int, C.c_int, i32p, C.c_int, f64p, f64p, C.c_int,
                                        C.c_int, i32p, C.c_int64, f64p, C.c_int64,
                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64),
-                                       C.POINTER(C.c_int)]
+                                       C.POINTER(C.c_int), C.c_void_p]
     lib.qtng_simulate_widths.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int,
                                          i32p, C.c_int, C.POINTER(C.c_int)]
     lib.qtng_edge_costs.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, f64p]
@@ -71,9 +79,16 @@ def _load():
                                            C.POINTER(Record), C.c_int, C.POINTER(C.c_int),
                                            C.POINTER(C.c_uint64)]
     lib.qtng_energy.argtypes = [vp, C.c_int, C.c_int, i32p, C.c_int, f64p, f64p, C.c_int,
-                                C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_double), f64p]
+                                C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_double),
+                                f64p, C.POINTER(EnergyReport)]
+    lib.qtng_energy_multi.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, i32p,
+                                      C.c_int, f64p, f64p, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(C.c_double), f64p, f32p]
+    lib.qtng_shard_edges.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int, i32p]
     lib.qtng_plan_create.argtypes = [vp, C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int,
-                                     C.c_int, C.c_void_p, pvp]
+                                     C.c_int, C.c_int, C.c_void_p, pvp]
+    lib.qtng_plan_terms.argtypes = [vp, f64p]
+    lib.qtng_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.qtng_plan_create_schedule.argtypes = [vp, C.c_int, i32p, C.c_int64, f64p, C.c_int, pvp]
     lib.qtng_plan_execute.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(C.c_float)]
@@ -104,7 +119,7 @@ lib = _load()
 EXPORTED = [
     "qtng_create", "qtng_destroy", "qtng_last_error", "qtng_version", "qtng_random_regular",
     "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_edge_work", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
-    "qtng_contract_schedule", "qtng_energy", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute",
+    "qtng_contract_schedule", "qtng_energy", "qtng_energy_multi", "qtng_shard_edges", "qtng_plan_terms", "qtng_fp64_peak", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute",
     "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_kernel_launches", "qtng_set_precision", "qtng_statevector_energy", "qtng_plan_segments", "qtng_plan_records", "qtng_plan_level_ms", "qtng_plan_kernel_ms",
     "qtng_plan_destroy", "qtng_plan_time_level",
 ]

@@ -3,6 +3,8 @@
 #include "qtng.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -12,6 +14,8 @@
 #include <cstdlib>
 #include <complex>
 #include <cstring>
+#include <limits>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -23,6 +27,10 @@
 #include "plan.hpp"
 #include "pool.hpp"
 #include "sv.cuh"
+
+namespace qtng {
+cudaError_t fp64_peak(int device, double* mul_add_ops_per_s, double* fma_flops_per_s);  // peak.cu
+}
 
 using namespace qtng;
 
@@ -154,6 +162,7 @@ WalkResult device_walk(const Schedule& s, int max_width, bool route = true) {
 struct ConeSet {
   std::vector<WalkResult> walks;
   std::vector<Edge> edges;
+  std::vector<int> merges_applied, merges_skipped;  // per lightcone (merge_buckets)
 };
 
 ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std::vector<int>& sel) {
@@ -161,6 +170,8 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
   const int k = static_cast<int>(sel.size());
   cs.walks.resize(k);
   cs.edges.resize(k);
+  cs.merges_applied.assign(k, 0);
+  cs.merges_skipped.assign(k, 0);
   std::vector<std::string> errs(k);
   std::vector<int> codes(k, 0);
   auto work = [&](int i) {
@@ -169,9 +180,17 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
       cs.edges[i] = e;
       Schedule s = edge_schedule(g, e, p);
       if (merged) s = merge_buckets(s);
+      cs.merges_applied[i] = s.merges_applied;
+      cs.merges_skipped[i] = s.merges_skipped;
       cs.walks[i] = device_walk(s, max_width);
     } catch (const Error& ex) {
       codes[i] = ex.code;
+      errs[i] = ex.what();
+    } catch (const std::bad_alloc&) {  // a worker thread must not terminate the process
+      codes[i] = kResource;
+      errs[i] = "host allocation failed";
+    } catch (const std::exception& ex) {
+      codes[i] = kInvalidInput;
       errs[i] = ex.what();
     }
   };
@@ -184,7 +203,7 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
 // Descriptor image of a HostPlan: one contiguous blob, 256-byte aligned sections.
 struct DescLayout {
   size_t ops = 0, ibeg = 0, trefs = 0, segs = 0, seg_ibeg = 0, stages = 0, ctr = 0, scal = 0,
-         lcb = 0, terms = 0, funits = 0, finit = 0, upload = 0, segtab = 0, fdone = 0, fdeps = 0,
+         lcb = 0, lce = 0, terms = 0, funits = 0, finit = 0, upload = 0, segtab = 0, fdone = 0, fdeps = 0,
          fqueue = 0, fstate = 0, total = 0;
 };
 
@@ -202,6 +221,7 @@ DescLayout layout_of(const HostPlan& hp) {
   L.ctr = o; o = align256(o + hp.levels.size() * 2 * sizeof(uint32_t));
   L.scal = o; o = align256(o + hp.scalar_off.size() * sizeof(uint64_t));
   L.lcb = o; o = align256(o + hp.lc_begin.size() * sizeof(uint32_t));
+  L.lce = o; o = align256(o + hp.lc_edge.size() * sizeof(int32_t));
   L.terms = o; o = align256(o + (hp.lc_begin.size()) * sizeof(double2));
   L.funits = o; o = align256(o + hp.flow_units.size() * sizeof(FlowUnit));
   L.finit = o; o = align256(o + hp.flow_init.size() * sizeof(uint64_t));
@@ -228,6 +248,7 @@ void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
   std::memcpy(dst + L.finit, hp.flow_init.data(), hp.flow_init.size() * sizeof(uint64_t));
   std::memcpy(dst + L.scal, hp.scalar_off.data(), hp.scalar_off.size() * sizeof(uint64_t));
   std::memcpy(dst + L.lcb, hp.lc_begin.data(), hp.lc_begin.size() * sizeof(uint32_t));
+  std::memcpy(dst + L.lce, hp.lc_edge.data(), hp.lc_edge.size() * sizeof(int32_t));
 }
 
 }  // namespace
@@ -243,6 +264,7 @@ struct Lane {
   DevBuf* arena = nullptr;
   DevBuf* desc = nullptr;
   PinBuf *pin_desc = nullptr, *pin_in = nullptr, *pin_out = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // device time of the lane's program (one-shot energy)
 };
 
 struct qtng_ctx {
@@ -258,11 +280,14 @@ struct qtng_ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, join3_ev = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf sv_scratch;     // state-vector oracle: edge bits, per-edge sums, partials
+  DevBuf multi_full;     // qtng_energy_multi: the 2m-double term vector NCCL reduces
   static constexpr int kLanes = 4;
   Lane lane[kLanes];     // lane 0 aliases the fields above; lanes 1.. own theirs
   DevBuf arena_x[kLanes], desc_x[kLanes];
   PinBuf pin_desc_x[kLanes], pin_in_x[kLanes], pin_out_x[kLanes];
-  int prec = 128;        // QAOA plans / energies: 128 = complex128, 64 = complex64
+  // default arithmetic of QAOA plans / energies whose call passes precision 0:
+  // 128 = complex128, 64 = complex64.  Read once per call (atomic).
+  std::atomic<int> prec{128};
 
   // arena of `elems` elements of `elem_bytes` (16: double2, 8: float2)
   void ensure_arena(uint64_t elems, size_t elem_bytes = sizeof(double2)) {
@@ -298,6 +323,7 @@ struct DevProgram {
   uint32_t* ctr(size_t level) const { return reinterpret_cast<uint32_t*>(base + L.ctr) + 2 * level; }
   const uint64_t* scal() const { return reinterpret_cast<const uint64_t*>(base + L.scal); }
   const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
+  const int32_t* lce() const { return reinterpret_cast<const int32_t*>(base + L.lce); }
   double2* terms() const { return reinterpret_cast<double2*>(base + L.terms); }
 };
 
@@ -371,9 +397,12 @@ void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* d
 // per-lightcone products.
 int launches_per_run(const HostPlan& hp);
 
+// full (optional, device, 2 doubles per edge of the graph): every lightcone's
+// term is also written to its edge slot (the multi-GPU reduce vector).
 void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, void* arena,
                      std::vector<cudaEvent_t>* level_events,
-                     std::vector<cudaEvent_t>* kernel_events = nullptr, const Lane* ln = nullptr) {
+                     std::vector<cudaEvent_t>* kernel_events = nullptr, const Lane* ln = nullptr,
+                     double2* full = nullptr) {
   const Lane& la = ln ? *ln : ctx->lane[0];
   cudaStream_t s = la.s;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -400,8 +429,8 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, vo
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
   QTNG_CUDA((pr.c64 ? c64::launch_final : c128::launch_final)(
-      s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1,
-                         arena, pr.terms()));
+      s, pr.scal(), pr.lcb(), static_cast<int>(hp.lc_begin.size()) - 1, arena, pr.terms(),
+      pr.lce(), full));
 }
 
 int launches_per_run(const HostPlan& hp) {
@@ -419,6 +448,16 @@ int launches_per_run(const HostPlan& hp) {
 // |imag e_jk| bound: the reference's 1e-8 (engine.cpp:517-519); complex64
 // plans use the north_star's 1e-5.
 double imag_tol(bool c64) { return c64 ? 1e-5 : 1e-8; }
+
+// The arithmetic of a QAOA plan / energy call: `precision` 0 = the context's
+// default (qtng_set_precision), read once.
+int resolve_prec(const qtng_ctx* ctx, int precision) {
+  if (precision == 0) return ctx->prec.load();
+  if (precision != 128 && precision != 64)
+    throw Error(kInvalidInput, "precision must be 128 or 64 bits");
+  return precision;
+}
+
 
 void check_terms(const std::vector<Edge>& edges, const double* terms, double tol = 1e-8) {
   for (size_t i = 0; i < edges.size(); ++i)
@@ -481,6 +520,8 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
     Lane& l0 = ctx->lane[0];
     l0 = Lane{ctx->stream, ctx->stream2, ctx->stream3, ctx->fork_ev, ctx->join_ev, ctx->join3_ev,
               &ctx->arena, &ctx->desc, &ctx->pin_desc, &ctx->pin_in, &ctx->pin_out};
+    for (int i = 0; i < qtng_ctx::kLanes; ++i)
+      for (cudaEvent_t* ev : {&ctx->lane[i].t0, &ctx->lane[i].t1}) QTNG_CUDA(cudaEventCreate(ev));
     for (int i = 1; i < qtng_ctx::kLanes; ++i) {
       Lane& l1 = ctx->lane[i];
       l1.arena = &ctx->arena_x[i];
@@ -515,6 +556,9 @@ void qtng_destroy(qtng_ctx* ctx) {
     for (cudaEvent_t e : {l1.fork, l1.join2, l1.join3})
       if (e) cudaEventDestroy(e);
   }
+  for (int i = 0; i < qtng_ctx::kLanes; ++i)
+    for (cudaEvent_t e : {ctx->lane[i].t0, ctx->lane[i].t1})
+      if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev})
     if (e) cudaEventDestroy(e);
   delete ctx;  // frees the arenas and staging buffers
@@ -526,8 +570,7 @@ qtng_status qtng_set_precision(qtng_ctx* ctx, int bits) {
   return guarded([&] {
     if (!ctx) throw Error(kInvalidInput, "null context");
     if (bits != 128 && bits != 64) throw Error(kInvalidInput, "precision must be 128 or 64 bits");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    ctx->prec = bits;
+    ctx->prec.store(bits);
   });
 }
 
@@ -547,7 +590,7 @@ qtng_status qtng_random_regular(int n, int d, uint64_t seed, int* edges, int cap
 qtng_status qtng_edge_schedule(int n, int m, const int* edges, int p, const double* gammas,
                                const double* betas, int edge_index, int merged, int* ints,
                                int64_t int_cap, double* data, int64_t data_cap,
-                               int64_t* n_ints, int64_t* n_data, int* n_buckets) {
+                               int64_t* n_ints, int64_t* n_data, int* n_buckets, int* merges) {
   return guarded([&] {
     validate_angles(p, gammas, betas);
     const Graph g = graph_from(n, m, edges);
@@ -562,6 +605,10 @@ qtng_status qtng_edge_schedule(int n, int m, const int* edges, int p, const doub
     *n_ints = static_cast<int64_t>(iv.size());
     *n_data = static_cast<int64_t>(dv.size());
     *n_buckets = static_cast<int>(s.buckets.size());
+    if (merges) {
+      merges[0] = s.merges_applied;
+      merges[1] = s.merges_skipped;
+    }
     if (static_cast<int64_t>(iv.size()) <= int_cap && static_cast<int64_t>(dv.size()) <= data_cap) {
       std::copy(iv.begin(), iv.end(), ints);
       std::copy(dv.begin(), dv.end(), data);
@@ -690,38 +737,6 @@ void run_program_once(qtng_ctx* ctx, const HostPlan& hp, const double* input,
   }
 }
 
-// One half of a pipelined energy on `la`: inputs (gate table) and
-// descriptors uploaded, the program enqueued, its terms copied back into the
-// lane's pinned buffer -- all asynchronous on the lane's main stream.
-void enqueue_energy_chunk(qtng_ctx* ctx, Lane& la, bool lane0, const HostPlan& hp,
-                          const double* table) {
-  const DescLayout L = layout_of(hp);
-  const size_t eb = elem_bytes(hp);
-  const uint64_t elems = std::max(hp.arena_elems, hp.input_elems);
-  if (lane0) {
-    ctx->ensure_arena(elems, eb);
-  } else if (std::max<uint64_t>(elems, 32) * eb > la.arena->cap) {
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    if (std::max<uint64_t>(elems, 32) * eb > free_b + la.arena->cap)
-      throw Error(kResource, "device arena of " + std::to_string(elems * eb) +
-                                 " bytes exceeds free HBM (" + std::to_string(free_b) + ")");
-    QTNG_CUDA(cudaStreamSynchronize(la.s));
-    la.arena->ensure(std::max<uint64_t>(elems, 32) * eb);
-  }
-  la.desc->ensure(L.total);
-  la.pin_in->ensure(std::max<uint64_t>(hp.input_elems, 1) * eb);
-  stage_input(hp, table, hp.input_elems, la.pin_in->p);
-  QTNG_CUDA(cudaMemcpyAsync(la.arena->p, la.pin_in->p, hp.input_elems * eb, cudaMemcpyHostToDevice,
-                            la.s));
-  upload_desc(ctx, hp, L, static_cast<char*>(la.desc->p), &la);
-  const DevProgram pr{static_cast<char*>(la.desc->p), L, hp.c64};
-  enqueue_program(ctx, hp, pr, la.arena->p, nullptr, nullptr, &la);
-  const size_t nb = (hp.lc_begin.size() - 1) * sizeof(double2);
-  la.pin_out->ensure(std::max<size_t>(nb, 16));
-  QTNG_CUDA(cudaMemcpyAsync(la.pin_out->p, pr.terms(), nb, cudaMemcpyDeviceToHost, la.s));
-}
-
 }  // namespace
 
 qtng_status qtng_contract_bucket(qtng_ctx* ctx, int n_tensors, const int* ranks, const int* vars,
@@ -819,10 +834,12 @@ qtng_status qtng_contract_schedule(qtng_ctx* ctx, int n_buckets, const int* ints
 // ---------------------------------------------------------------- plans
 
 qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int p, int merged,
-                             int max_result_width, int n_sel, const int* sel, qtng_plan** out) {
+                             int max_result_width, int precision, int n_sel, const int* sel,
+                             qtng_plan** out) {
   return guarded([&] {
     if (!ctx || !out) throw Error(kInvalidInput, "null argument");
     if (p < 1) throw Error(kInvalidInput, "angles: gammas and betas must have equal length p >= 1");
+    const int prec = resolve_prec(ctx, precision);
     const Graph g = graph_from(n, m, edges);
     const std::vector<int> s = selection(m, n_sel, sel);
     ConeSet cs = plan_cones(g, p, merged != 0, max_result_width, s);
@@ -837,7 +854,7 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
     std::vector<const WalkResult*> ptrs;
     for (const WalkResult& w : cs.walks) ptrs.push_back(&w);
     plan->hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
-    plan->hp.c64 = ctx->prec == 64;
+    plan->hp.c64 = prec == 64;
     const HostPlan& hp = plan->hp;
     const DescLayout L = layout_of(hp);
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1185,90 +1202,450 @@ qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* le
 
 // ---------------------------------------------------------------- energy (end to end)
 
+}  // extern "C"
+
+namespace {
+
+// One device's share of energy_expectation (engine.cpp:503-563): the terms,
+// refusals and report data of the selected lightcones.
+struct EnergyRun {
+  std::vector<double> t;          // (re, im) per selected edge, selection order
+  std::vector<std::string> fail;  // per selected edge: refusal message ("" = contracted)
+  std::vector<Edge> edge_at;
+  uint64_t peak = 0;              // max over lightcones of 16 << largest result rank
+  int merges_applied = 0, merges_skipped = 0;
+  float device_ms = 0.f;          // sum over lanes of their program's device time
+  std::vector<qtng_record> recs;  // want_records: one per contracted bucket, selection order
+};
+
+// On an error path, every lane already enqueued is synchronised before the
+// context lock is released: its copies and kernels still use the lane buffers.
+struct LaneGuard {
+  qtng_ctx* ctx;
+  int n = 0;
+  ~LaneGuard() {
+    for (int c = 0; c < n; ++c) cudaStreamSynchronize(ctx->lane[c].s);
+  }
+};
+
+// Upload + run + copy back one lightcone chunk on lane `la` (all asynchronous).
+void enqueue_energy_chunk_timed(qtng_ctx* ctx, Lane& la, bool lane0, const HostPlan& hp,
+                                const double* table, double2* full) {
+  const DescLayout L = layout_of(hp);
+  const size_t eb = elem_bytes(hp);
+  const uint64_t elems = std::max(hp.arena_elems, hp.input_elems);
+  if (lane0) {
+    ctx->ensure_arena(elems, eb);
+  } else if (std::max<uint64_t>(elems, 32) * eb > la.arena->cap) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (std::max<uint64_t>(elems, 32) * eb > free_b + la.arena->cap)
+      throw Error(kResource, "device arena of " + std::to_string(elems * eb) +
+                                 " bytes exceeds free HBM (" + std::to_string(free_b) + ")");
+    QTNG_CUDA(cudaStreamSynchronize(la.s));
+    la.arena->ensure(std::max<uint64_t>(elems, 32) * eb);
+  }
+  la.desc->ensure(L.total);
+  la.pin_in->ensure(std::max<uint64_t>(hp.input_elems, 1) * eb);
+  stage_input(hp, table, hp.input_elems, la.pin_in->p);
+  QTNG_CUDA(cudaMemcpyAsync(la.arena->p, la.pin_in->p, hp.input_elems * eb, cudaMemcpyHostToDevice,
+                            la.s));
+  upload_desc(ctx, hp, L, static_cast<char*>(la.desc->p), &la);
+  const DevProgram pr{static_cast<char*>(la.desc->p), L, hp.c64};
+  QTNG_CUDA(cudaEventRecord(la.t0, la.s));
+  enqueue_program(ctx, hp, pr, la.arena->p, nullptr, nullptr, &la, full);
+  QTNG_CUDA(cudaEventRecord(la.t1, la.s));
+  const size_t nb = (hp.lc_begin.size() - 1) * sizeof(double2);
+  la.pin_out->ensure(std::max<size_t>(nb, 16));
+  QTNG_CUDA(cudaMemcpyAsync(la.pin_out->p, pr.terms(), nb, cudaMemcpyDeviceToHost, la.s));
+}
+
+// The selected lightcones `s` on ctx: host planning of chunk c+1 overlaps the
+// device work of chunks <= c (K lanes, QTNG_PIPELINE).  full (optional,
+// device, 2 doubles per graph edge, zeroed here): every contracted term is also
+// written to its edge slot (the multi-GPU reduce vector).  Refusals are
+// returned in `out.fail`, not thrown.
+void energy_run(qtng_ctx* ctx, const Graph& g, int p, const double* gammas, const double* betas,
+                bool merged, int max_result_width, int prec, const std::vector<int>& s,
+                bool want_records, double2* full, EnergyRun& out) {
+  PhaseTimer tm("qtng_energy");
+  static const int lanes = [] {
+    const char* v = std::getenv("QTNG_PIPELINE");  // lanes (1 = no pipelining)
+    const int x = v ? std::atoi(v) : 3;
+    return std::max(1, std::min(x, qtng_ctx::kLanes));
+  }();
+  const int K = std::max(1, std::min<int>(lanes, static_cast<int>(s.size()) / 4));
+  std::vector<std::vector<int>> pos(K), part(K);  // positions in s, edge indices
+  for (size_t i = 0; i < s.size(); ++i) {
+    pos[i % K].push_back(static_cast<int>(i));
+    part[i % K].push_back(s[i]);
+  }
+  std::vector<ConeSet> cs(K);
+  std::vector<HostPlan> hps(K);
+  std::vector<std::vector<int>> okpos(K);  // positions (in s) of the contracted lightcones
+  out.t.assign(2 * s.size(), 0.0);
+  out.fail.assign(s.size(), std::string());
+  out.edge_at.assign(s.size(), Edge{});
+  std::vector<double> table;
+  std::unique_lock<std::mutex> lk(ctx->mu, std::defer_lock);
+  LaneGuard guard{ctx, 0};
+  for (int c = 0; c < K; ++c) {
+    cs[c] = plan_cones(g, p, merged, max_result_width, part[c]);
+    std::vector<const WalkResult*> ok;
+    for (size_t k = 0; k < cs[c].walks.size(); ++k) {
+      const int at = pos[c][k];
+      const WalkResult& w = cs[c].walks[k];
+      out.edge_at[at] = cs[c].edges[k];
+      out.merges_applied += cs[c].merges_applied[k];
+      out.merges_skipped += cs[c].merges_skipped[k];
+      if (w.fail_code) {
+        out.fail[at] = w.fail_msg.empty() ? std::string("refused") : w.fail_msg;
+      } else {
+        ok.push_back(&w);
+        okpos[c].push_back(at);
+        if (!w.ops.empty()) out.peak = std::max(out.peak, uint64_t{16} << w.max_result_rank);
+      }
+    }
+    tm.mark("schedules+walks");
+    if (ok.empty()) continue;
+    hps[c] = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
+    hps[c].c64 = prec == 64;
+    for (size_t k = 0; k < okpos[c].size(); ++k) hps[c].lc_edge[k] = s[okpos[c][k]];
+    tm.mark("build_plan");
+    if (table.empty()) {
+      table.resize(2 * hps[c].input_elems);
+      fill_gate_table(p, gammas, betas, table.data());
+    }
+    if (!lk.owns_lock()) {
+      lk.lock();
+      QTNG_CUDA(cudaSetDevice(ctx->device));
+      if (full) {  // before any lane's final kernel can write its slots
+        QTNG_CUDA(cudaMemsetAsync(full, 0, static_cast<size_t>(g.edges.size()) * sizeof(double2),
+                                  ctx->lane[0].s));
+        QTNG_CUDA(cudaStreamSynchronize(ctx->lane[0].s));
+      }
+    }
+    guard.n = c + 1;
+    enqueue_energy_chunk_timed(ctx, ctx->lane[c], c == 0, hps[c], table.data(), full);
+    tm.mark("upload+enqueue");
+  }
+  std::vector<float> lane_ms(K, 0.f);
+  for (int c = 0; c < K; ++c) {
+    if (okpos[c].empty()) continue;
+    QTNG_CUDA(cudaStreamSynchronize(ctx->lane[c].s));
+    QTNG_CUDA(cudaEventElapsedTime(&lane_ms[c], ctx->lane[c].t0, ctx->lane[c].t1));
+    out.device_ms += lane_ms[c];
+    const double* o = static_cast<const double*>(ctx->lane[c].pin_out->p);
+    for (size_t k = 0; k < okpos[c].size(); ++k) {
+      out.t[2 * okpos[c][k]] = o[2 * k];
+      out.t[2 * okpos[c][k] + 1] = o[2 * k + 1];
+    }
+  }
+  guard.n = 0;
+  tm.mark("device+d2h");
+  if (!want_records) return;
+  // TimingRecords (engine.cpp:275-282), selection order: elapsed_s is the
+  // bucket's share (by algorithmic bytes) of its lane's measured device time
+  // -- a fused level kernel runs hundreds of buckets at once, so per-bucket
+  // device times do not exist.
+  std::vector<std::pair<int, int>> at_of(s.size(), {-1, -1});  // position -> (chunk, lightcone)
+  for (int c = 0; c < K; ++c)
+    for (size_t k = 0; k < okpos[c].size(); ++k) at_of[okpos[c][k]] = {c, static_cast<int>(k)};
+  std::vector<double> chunk_bytes(K, 0.0);
+  for (int c = 0; c < K; ++c)
+    for (double b : hps[c].rec_bytes) chunk_bytes[c] += b;
+  for (size_t i = 0; i < s.size(); ++i) {
+    const auto [c, k] = at_of[i];
+    if (c < 0) continue;
+    const HostPlan& hp = hps[c];
+    for (uint32_t r = hp.rec_begin[k]; r < hp.rec_begin[k + 1]; ++r) {
+      qtng_record q{};
+      q.edge_u = out.edge_at[i].u;
+      q.edge_v = out.edge_at[i].v;
+      q.bucket_seq = hp.rec_seq[r];
+      q.width = hp.rec_width[r];
+      q.ops = uint64_t{1} << q.width;
+      const double share = chunk_bytes[c] > 0 ? hp.rec_bytes[r] / chunk_bytes[c] : 0.0;
+      q.elapsed_s = std::max(1e-9, 1e-3 * lane_ms[c] * share);
+      q.flops_est = 8.0 * static_cast<double>(q.ops) / q.elapsed_s;
+      out.recs.push_back(q);
+    }
+  }
+}
+
+// energy_expectation's failure rule (engine.cpp:517-519, 543-546): the first
+// refused or non-real lightcone in order raises ScheduleError("edge (u, v): ...").
+void raise_first_failure(const std::vector<std::string>& fail, const std::vector<Edge>& edge_at,
+                         const std::vector<double>& t, double tol) {
+  for (size_t i = 0; i < fail.size(); ++i) {
+    const bool refused = !fail[i].empty();
+    const bool complex_term = !refused && std::abs(t[2 * i + 1]) > tol;
+    if (refused || complex_term) {
+      const std::string what = refused ? fail[i]
+                                       : "edge term has non-real value: imag = " +
+                                             std::to_string(t[2 * i + 1]);
+      throw Error(kSchedule, "edge (" + std::to_string(edge_at[i].u) + ", " +
+                                 std::to_string(edge_at[i].v) + "): " + what);
+    }
+  }
+}
+
+bool selects_all_in_order(const std::vector<int>& s, int m) {
+  if (static_cast<int>(s.size()) != m) return false;
+  for (int i = 0; i < m; ++i)
+    if (s[i] != i) return false;
+  return true;
+}
+
+void fill_report(const EnergyRun& r, qtng_energy_report* rep) {
+  if (!rep) return;
+  rep->n_records = static_cast<int64_t>(r.recs.size());
+  rep->peak_tensor_bytes = r.peak;
+  rep->merges_applied = r.merges_applied;
+  rep->merges_skipped = r.merges_skipped;
+  rep->device_ms = r.device_ms;
+  if (rep->records)
+    for (int64_t i = 0; i < rep->rec_cap && i < rep->n_records; ++i) rep->records[i] = r.recs[i];
+}
+
+}  // namespace
+
+extern "C" {
+
 qtng_status qtng_energy(qtng_ctx* ctx, int n, int m, const int* edges, int p,
                         const double* gammas, const double* betas, int merged,
-                        int max_result_width, int n_sel, const int* sel, double* energy,
-                        double* terms) {
+                        int max_result_width, int precision, int n_sel, const int* sel,
+                        double* energy, double* terms, qtng_energy_report* report) {
   return guarded([&] {
     if (!ctx) throw Error(kInvalidInput, "null context");
     validate_angles(p, gammas, betas);
+    const int prec = resolve_prec(ctx, precision);
     const Graph g = graph_from(n, m, edges);
     const std::vector<int> s = selection(m, n_sel, sel);
-    PhaseTimer tm("qtng_energy");
-    // K lanes: lightcone chunk c+1 is planned on the host while chunks <= c
-    // run on the device (QTNG_PIPELINE=1: one program).
-    static const int lanes = [] {
-      const char* v = std::getenv("QTNG_PIPELINE");  // lanes (1 = no pipelining)
-      const int x = v ? std::atoi(v) : 3;
-      return std::max(1, std::min(x, qtng_ctx::kLanes));
-    }();
-    const int K = std::max(1, std::min<int>(lanes, static_cast<int>(s.size()) / 4));
-    std::vector<std::vector<int>> pos(K), part(K);  // positions in s, edge indices
-    for (size_t i = 0; i < s.size(); ++i) {
-      pos[i % K].push_back(static_cast<int>(i));
-      part[i % K].push_back(s[i]);
-    }
-    std::vector<ConeSet> cs(K);
-    std::vector<HostPlan> hps(K);
-    std::vector<std::vector<int>> okpos(K);  // positions (in s) of the contracted lightcones
-    std::vector<const WalkResult*> failed(s.size(), nullptr);
-    std::vector<Edge> edge_at(s.size());
-    std::vector<double> table;
-    std::unique_lock<std::mutex> lk(ctx->mu, std::defer_lock);
-    for (int c = 0; c < K; ++c) {
-      cs[c] = plan_cones(g, p, merged != 0, max_result_width, part[c]);
-      std::vector<const WalkResult*> ok;
-      for (size_t k = 0; k < cs[c].walks.size(); ++k) {
-        edge_at[pos[c][k]] = cs[c].edges[k];
-        if (cs[c].walks[k].fail_code) {
-          failed[pos[c][k]] = &cs[c].walks[k];
-        } else {
-          ok.push_back(&cs[c].walks[k]);
-          okpos[c].push_back(pos[c][k]);
-        }
-      }
-      tm.mark("schedules+walks");
-      if (ok.empty()) continue;
-      hps[c] = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
-      hps[c].c64 = ctx->prec == 64;
-      tm.mark("build_plan");
-      if (table.empty()) {
-        table.resize(2 * hps[c].input_elems);
-        fill_gate_table(p, gammas, betas, table.data());
-      }
-      if (!lk.owns_lock()) {
-        lk.lock();
-        QTNG_CUDA(cudaSetDevice(ctx->device));
-      }
-      enqueue_energy_chunk(ctx, ctx->lane[c], c == 0, hps[c], table.data());
-      tm.mark("upload+enqueue");
-    }
-    std::vector<double> t(2 * s.size(), 0.0);
-    for (int c = 0; c < K; ++c) {
-      if (okpos[c].empty()) continue;
-      QTNG_CUDA(cudaStreamSynchronize(ctx->lane[c].s));
-      const double* o = static_cast<const double*>(ctx->lane[c].pin_out->p);
-      for (size_t k = 0; k < okpos[c].size(); ++k) {
-        t[2 * okpos[c][k]] = o[2 * k];
-        t[2 * okpos[c][k] + 1] = o[2 * k + 1];
-      }
-    }
-    tm.mark("device+d2h");
-    for (size_t i = 0; i < s.size(); ++i) {
-      const bool refused = failed[i] != nullptr;
-      const bool complex_term = !refused && std::abs(t[2 * i + 1]) > imag_tol(ctx->prec == 64);
-      if (refused || complex_term) {
-        const std::string what = refused ? failed[i]->fail_msg
-                                         : "edge term has non-real value: imag = " +
-                                               std::to_string(t[2 * i + 1]);
-        throw Error(kSchedule, "edge (" + std::to_string(edge_at[i].u) + ", " +
-                                   std::to_string(edge_at[i].v) + "): " + what);
-      }
-    }
+    EnergyRun r;
+    energy_run(ctx, g, p, gammas, betas, merged != 0, max_result_width, prec, s,
+               report && report->records, nullptr, r);
+    raise_first_failure(r.fail, r.edge_at, r.t, imag_tol(prec == 64));
     double sum = 0.0;  // edge order, like engine.cpp:549-551
-    for (size_t i = 0; i < s.size(); ++i) sum += t[2 * i];
+    for (size_t i = 0; i < s.size(); ++i) sum += r.t[2 * i];
+    // a partial selection has no energy (its terms are the result)
+    if (energy)
+      *energy = selects_all_in_order(s, m) ? 0.5 * static_cast<double>(m) - 0.5 * sum
+                                           : std::numeric_limits<double>::quiet_NaN();
+    if (terms) std::copy(r.t.begin(), r.t.end(), terms);
+    fill_report(r, report);
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- multi-GPU driver
+
+namespace {
+
+// NCCL, resolved at first use (the library is loaded by soname, so a process
+// that already holds torch's NCCL shares it; nothing links against it).
+struct NcclApi {
+  decltype(&ncclCommInitAll) init_all = nullptr;
+  decltype(&ncclReduce) reduce = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  std::string missing;
+
+  static const NcclApi& get() {
+    static const NcclApi api = [] {
+      NcclApi a;
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) {
+        a.missing = std::string("NCCL unavailable: ") + dlerror();
+        return a;
+      }
+      a.init_all = reinterpret_cast<decltype(a.init_all)>(dlsym(h, "ncclCommInitAll"));
+      a.reduce = reinterpret_cast<decltype(a.reduce)>(dlsym(h, "ncclReduce"));
+      a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+      a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+      a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+      if (!a.init_all || !a.reduce || !a.group_start || !a.group_end || !a.error_string)
+        a.missing = "NCCL unavailable: missing symbols in libnccl.so.2";
+      return a;
+    }();
+    if (!api.missing.empty()) throw Error(kCuda, api.missing);
+    return api;
+  }
+};
+
+#define QTNG_NCCL(api, call)                                                        \
+  do {                                                                              \
+    const ncclResult_t r_ = (call);                                                 \
+    if (r_ != ncclSuccess) throw Error(kCuda, std::string(#call) + ": " + (api).error_string(r_)); \
+  } while (0)
+
+// One communicator set per device list, created on first use and kept for
+// the life of the process (ncclCommInitAll costs far more than an energy).
+std::vector<ncclComm_t> comms_for(const std::vector<int>& devs) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, std::vector<ncclComm_t>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(devs);
+  if (it != cache.end()) return it->second;
+  const NcclApi& nc = NcclApi::get();
+  std::vector<ncclComm_t> c(devs.size());
+  QTNG_NCCL(nc, nc.init_all(c.data(), static_cast<int>(devs.size()), devs.data()));
+  cache[devs] = c;
+  return c;
+}
+
+// LPT (longest processing time first) placement of the lightcones on
+// n_shards devices by predicted work (qtng_edge_work): edges by decreasing
+// work (ties: lower index) onto the least-loaded shard (ties: lower shard).
+std::vector<int> lpt_owner(const std::vector<double>& work, int n_shards) {
+  const int m = static_cast<int>(work.size());
+  std::vector<int> order(m);
+  for (int i = 0; i < m; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+  std::vector<double> load(n_shards, 0.0);
+  std::vector<int> owner(m, 0);
+  for (int i : order) {
+    const int r = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+    owner[i] = r;
+    load[r] += work[i];
+  }
+  return owner;
+}
+
+std::vector<double> predicted_work(const Graph& g, int p, bool merged) {
+  const int m = static_cast<int>(g.edges.size());
+  const ConeSet cs = plan_cones(g, p, merged, 1 << 20, selection(m, m, nullptr));
+  std::vector<double> work(m, 0.0);
+  for (int i = 0; i < m; ++i)
+    for (const Op& op : cs.walks[i].ops)  // the reference loop's complex products + additions
+      work[i] += std::ldexp(1.0, op.width) * std::max(1, op.nin - 1) +
+                 std::ldexp(1.0, op.r) * (std::ldexp(1.0, op.ns) - 1.0);
+  return work;
+}
+
+}  // namespace
+
+extern "C" {
+
+qtng_status qtng_shard_edges(int n, int m, const int* edges, int p, int merged, int n_shards,
+                             int* owner) {
+  return guarded([&] {
+    if (n_shards < 1 || !owner) throw Error(kInvalidInput, "invalid shard count");
+    const Graph g = graph_from(n, m, edges);
+    const std::vector<int> o = lpt_owner(predicted_work(g, p, merged != 0), n_shards);
+    std::copy(o.begin(), o.end(), owner);
+  });
+}
+
+qtng_status qtng_energy_multi(qtng_ctx* const* ctxs, int n_ctx, int n, int m, const int* edges,
+                              int p, const double* gammas, const double* betas, int merged,
+                              int max_result_width, int precision, double* energy, double* terms,
+                              float* shard_ms) {
+  return guarded([&] {
+    if (!ctxs || n_ctx < 1) throw Error(kInvalidInput, "no contexts");
+    std::vector<int> devs(n_ctx);
+    for (int i = 0; i < n_ctx; ++i) {
+      if (!ctxs[i]) throw Error(kInvalidInput, "null context");
+      devs[i] = ctxs[i]->device;
+      for (int j = 0; j < i; ++j)
+        if (devs[j] == devs[i]) throw Error(kInvalidInput, "contexts must be on distinct devices");
+    }
+    validate_angles(p, gammas, betas);
+    const int prec = resolve_prec(ctxs[0], precision);
+    const Graph g = graph_from(n, m, edges);
+    const std::vector<int> owner = lpt_owner(predicted_work(g, p, merged != 0), n_ctx);
+    std::vector<std::vector<int>> shard(n_ctx);
+    for (int i = 0; i < m; ++i) shard[owner[i]].push_back(i);  // ascending edge order
+    for (int r = 0; r < n_ctx; ++r) {
+      std::lock_guard<std::mutex> lk(ctxs[r]->mu);
+      QTNG_CUDA(cudaSetDevice(ctxs[r]->device));
+      ctxs[r]->multi_full.ensure(std::max<size_t>(1, m) * sizeof(double2));
+    }
+    // one host thread per device: plan + contract the shard, terms scattered
+    // into the device's reduce vector by the final kernel
+    std::vector<EnergyRun> runs(n_ctx);
+    std::vector<std::exception_ptr> errs(n_ctx);
+    auto work = [&](int r) {
+      try {
+        if (shard[r].empty()) {  // nothing to contract: a zero vector joins the reduce
+          std::lock_guard<std::mutex> lk(ctxs[r]->mu);
+          QTNG_CUDA(cudaSetDevice(ctxs[r]->device));
+          QTNG_CUDA(cudaMemset(ctxs[r]->multi_full.p, 0, std::max<size_t>(1, m) * sizeof(double2)));
+          return;
+        }
+        energy_run(ctxs[r], g, p, gammas, betas, merged != 0, max_result_width, prec, shard[r],
+                   false, static_cast<double2*>(ctxs[r]->multi_full.p), runs[r]);
+      } catch (...) {
+        errs[r] = std::current_exception();
+      }
+    };
+    std::vector<std::thread> th;
+    for (int r = 1; r < n_ctx; ++r) th.emplace_back(work, r);
+    work(0);
+    for (std::thread& t : th) t.join();
+    for (const std::exception_ptr& e : errs)
+      if (e) std::rethrow_exception(e);
+    // the single collective: sum-reduce the 2m-double vectors onto ctxs[0]
+    const std::vector<ncclComm_t> comms = comms_for(devs);
+    const NcclApi& nc = NcclApi::get();
+    std::vector<std::unique_lock<std::mutex>> locks;
+    std::vector<int> by_addr(n_ctx);
+    for (int r = 0; r < n_ctx; ++r) by_addr[r] = r;
+    std::sort(by_addr.begin(), by_addr.end(), [&](int a, int b) { return ctxs[a] < ctxs[b]; });
+    for (int r : by_addr) locks.emplace_back(ctxs[r]->mu);  // fixed order: no deadlock
+    QTNG_NCCL(nc, nc.group_start());
+    for (int r = 0; r < n_ctx; ++r) {
+      QTNG_CUDA(cudaSetDevice(ctxs[r]->device));
+      void* buf = ctxs[r]->multi_full.p;
+      QTNG_NCCL(nc, nc.reduce(buf, buf, 2 * static_cast<size_t>(m), ncclFloat64, ncclSum, 0,
+                              comms[r], ctxs[r]->stream));
+    }
+    QTNG_NCCL(nc, nc.group_end());
+    std::vector<double> full(2 * static_cast<size_t>(m), 0.0);
+    QTNG_CUDA(cudaSetDevice(ctxs[0]->device));
+    if (m > 0)
+      QTNG_CUDA(cudaMemcpyAsync(full.data(), ctxs[0]->multi_full.p, full.size() * sizeof(double),
+                                cudaMemcpyDeviceToHost, ctxs[0]->stream));
+    for (int r = 0; r < n_ctx; ++r) {
+      QTNG_CUDA(cudaSetDevice(ctxs[r]->device));
+      QTNG_CUDA(cudaStreamSynchronize(ctxs[r]->stream));
+    }
+    locks.clear();
+    // failures and terms in edge order (engine.cpp:543-551)
+    std::vector<std::string> fail(m);
+    std::vector<Edge> edge_at(g.edges.begin(), g.edges.end());
+    for (int r = 0; r < n_ctx; ++r)
+      for (size_t k = 0; k < runs[r].fail.size(); ++k) fail[shard[r][k]] = runs[r].fail[k];
+    raise_first_failure(fail, edge_at, full, imag_tol(prec == 64));
+    double sum = 0.0;
+    for (int i = 0; i < m; ++i) sum += full[2 * i];
     if (energy) *energy = 0.5 * static_cast<double>(m) - 0.5 * sum;
-    if (terms) std::copy(t.begin(), t.end(), terms);
+    if (terms) std::copy(full.begin(), full.end(), terms);
+    if (shard_ms)
+      for (int r = 0; r < n_ctx; ++r) shard_ms[r] = runs[r].device_ms;
+  });
+}
+
+qtng_status qtng_fp64_peak(int device, double* mul_add_ops_per_s, double* fma_flops_per_s) {
+  return guarded([&] {
+    if (!mul_add_ops_per_s || !fma_flops_per_s) throw Error(kInvalidInput, "null argument");
+    QTNG_CUDA(fp64_peak(device, mul_add_ops_per_s, fma_flops_per_s));
+  });
+}
+
+qtng_status qtng_plan_terms(qtng_plan* plan, double* terms) {
+  return guarded([&] {
+    if (!plan || !terms) throw Error(kInvalidInput, "null argument");
+    qtng_ctx* ctx = plan->ctx;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    const size_t nb = plan->edges.size() * sizeof(double2);
+    QTNG_CUDA(cudaMemcpyAsync(plan->pin_terms.p, plan->prog.terms(), nb, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(terms, plan->pin_terms.p, nb);
   });
 }
 

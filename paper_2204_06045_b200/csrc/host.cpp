@@ -340,10 +340,13 @@ Schedule merge_buckets(const Schedule& schedule) {
       trial.buckets.erase(trial.buckets.begin() + static_cast<long>(i));
       const int mw = max_width_or_invalid(trial);
       if (mw >= 0 && mw <= budget) {
+        trial.merges_applied = sched.merges_applied + 1;
+        trial.merges_skipped = sched.merges_skipped;
         sched = std::move(trial);
         merged = true;
         break;
       }
+      ++sched.merges_skipped;
     }
     if (!merged) ++i;
   }

@@ -110,6 +110,10 @@ struct SchedBucket {
 struct Schedule {
   std::vector<SchedTensor> init;
   std::vector<SchedBucket> buckets;
+  // merge_buckets bookkeeping (ContractionSchedule::merges_applied/_skipped,
+  // proj/include/qtnsim/ordering.hpp; counted as engine.cpp:343-353 does)
+  int merges_applied = 0;
+  int merges_skipped = 0;
 };
 
 // assign_buckets (proj/src/ordering.cpp:44-68) for a QAOA network; initial

@@ -1253,7 +1253,8 @@ int seg_grid(uint32_t items) {
 // (complex128 arithmetic also for complex64 plans).
 __global__ void final_kernel(const uint64_t* __restrict__ scalar_off,
                              const uint32_t* __restrict__ lc_begin, int n_lc,
-                             const V* __restrict__ arena, double2* __restrict__ terms) {
+                             const V* __restrict__ arena, double2* __restrict__ terms,
+                             const int32_t* __restrict__ lc_edge, double2* __restrict__ full) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_lc) return;
   double2 s = make_double2(1.0, 0.0);  // report.scalar = 1 (engine.cpp:253)
@@ -1264,6 +1265,7 @@ __global__ void final_kernel(const uint64_t* __restrict__ scalar_off,
                      __dadd_rn(__dmul_rn(s.x, b.y), __dmul_rn(s.y, b.x)));
   }
   terms[i] = s;
+  if (full) full[lc_edge[i]] = s;
 }
 
 template <int MAXT>
@@ -1374,10 +1376,12 @@ cudaError_t launch_level(cudaStream_t s, const DevOp* ops, const uint32_t* ibeg,
 }
 
 cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint32_t* lc_begin,
-                         int n_lc, const void* arena_v, double2* terms) {
+                         int n_lc, const void* arena_v, double2* terms, const int32_t* lc_edge,
+                         double2* full) {
   if (n_lc <= 0) return cudaSuccess;
   const V* arena = static_cast<const V*>(arena_v);
-  final_kernel<<<(n_lc + 127) / 128, 128, 0, s>>>(scalar_off, lc_begin, n_lc, arena, terms);
+  final_kernel<<<(n_lc + 127) / 128, 128, 0, s>>>(scalar_off, lc_begin, n_lc, arena, terms,
+                                                  lc_edge, full);
   return cudaGetLastError();
 }
 

@@ -41,9 +41,11 @@ namespace qtng {
                           uint32_t* done, int32_t* deps, uint64_t* queue, FlowState* st);      \
   /* resident warps of the level kernel on the current device */                              \
   int resident_warps();                                                                        \
-  /* per lightcone: e_jk = prod of its scalar results in production order (complex128) */     \
+  /* per lightcone: e_jk = prod of its scalar results in production order (complex128); */   \
+  /* full (optional): also written to full[lc_edge[i]] (the multi-GPU reduce vector) */       \
   cudaError_t launch_final(cudaStream_t s, const uint64_t* scalar_off, const uint32_t* lc_begin, \
-                           int n_lc, const void* arena, double2* terms);
+                           int n_lc, const void* arena, double2* terms,                       \
+                           const int32_t* lc_edge, double2* full);
 
 namespace c128 {
 QTNG_KERNEL_API

@@ -728,6 +728,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     hp.rec_begin.push_back(static_cast<uint32_t>(hp.rec_seq.size()));
     for (int s : w.scalars) hp.scalar_off.push_back(out[base[c] + s]);
     hp.lc_begin.push_back(static_cast<uint32_t>(hp.scalar_off.size()));
+    hp.lc_edge.push_back(c);
   }
   ptm.mark("records");
   return hp;

@@ -36,6 +36,9 @@ struct HostPlan {
   double single_alg_bytes = 0;         // B_alg of the single (level/outer kernel) ops
   std::vector<uint64_t> scalar_off;    // per lightcone: its scalar results, production order
   std::vector<uint32_t> lc_begin;      // n_lightcones + 1 prefix into scalar_off
+  // per lightcone: its slot in the multi-GPU reduce vector (the edge index;
+  // build_plan sets 0..n-1, callers overwrite before the upload)
+  std::vector<int32_t> lc_edge;
   uint64_t input_elems = 0;
   uint64_t arena_elems = 0;            // peak arena size (elements)
   // accounting: B_alg = sum_in 16*2^rank + 16*2^r; ops = 2^width

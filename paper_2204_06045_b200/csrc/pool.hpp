@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <exception>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -22,7 +23,9 @@ class Pool {
   int size() const { return static_cast<int>(workers_.size()) + 1; }
 
   // fn(i) for i in [0, n), on the workers and the calling thread.  Calls from
-  // inside a task, or concurrent calls, run serially on the caller.
+  // inside a task, or concurrent calls, run serially on the caller.  An
+  // exception thrown by a task (on any thread) is rethrown here, on the
+  // caller, after every worker has left the loop (the first one wins).
   void parallel_for(int n, const std::function<void(int)>& fn) {
     if (n <= 0) return;
     std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
@@ -35,6 +38,7 @@ class Pool {
       fn_ = &fn;
       n_ = n;
       next_.store(0);
+      err_ = nullptr;
       active_ = static_cast<int>(workers_.size());
       gen_.fetch_add(1, std::memory_order_release);
     }
@@ -43,6 +47,11 @@ class Pool {
     std::unique_lock<std::mutex> lk(mu_);
     done_cv_.wait(lk, [&] { return active_ == 0; });
     fn_ = nullptr;
+    if (err_) {
+      std::exception_ptr e = err_;
+      err_ = nullptr;
+      std::rethrow_exception(e);
+    }
   }
 
  private:
@@ -60,7 +69,15 @@ class Pool {
     for (auto& t : workers_) t.join();
   }
   void drain() {
-    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*fn_)(i);
+    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) {
+      try {
+        (*fn_)(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(err_mu_);
+        if (!err_) err_ = std::current_exception();
+        next_.store(n_);  // stop handing out work
+      }
+    }
   }
   void loop() {
     uint64_t seen = 0;
@@ -86,7 +103,8 @@ class Pool {
     }
   }
   std::vector<std::thread> workers_;
-  std::mutex mu_, run_mu_;
+  std::mutex mu_, run_mu_, err_mu_;
+  std::exception_ptr err_;  // first task exception of the current loop
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* fn_ = nullptr;
   int n_ = 0;

@@ -1,4 +1,5 @@
-"""Multi-GPU driver: edge lightcones sharded over the GPUs of one node.
+"""Multi-GPU driver (torchrun flavour): edge lightcones sharded over the GPUs of
+one node, one process per GPU.
 
 Lightcones are independent (the reference already runs them on a thread pool,
 proj/src/engine.cpp:531-541), so the only exchange is one reduction of the
@@ -9,9 +10,12 @@ with a single NCCL reduce (sum), and rank 0 forms
 does (engine.cpp:549-560).  Summing a slot with zeros is exact, so the
 N-GPU energy is bit-identical to the 1-GPU one.
 
-Sharding is LPT (longest processing time first) on the predicted algorithmic
-bytes of every lightcone (qtng_edge_costs): the contraction is HBM-bound, so
-bytes predict device time.
+Sharding is LPT (longest processing time first) on the predicted device work
+of every lightcone (qtng_edge_work: complex products + adds of the reference
+loop).  The fused device program is bound by FP64 issue and latency, not by
+HBM bytes, so work -- not bytes -- predicts device time.  `shards_for` uses
+the library's own placement (qtng_shard_edges), the one the single-process
+C driver qtng_energy_multi uses, so both drivers shard identically.
 """
 from __future__ import annotations
 
@@ -34,6 +38,12 @@ def lpt_shard(costs: Sequence[float], world: int) -> List[List[int]]:
         out[r].append(i)
         heapq.heappush(heap, (load + float(costs[i]), r))
     return [sorted(s) for s in out]
+
+
+def shards_for(q, g, p: int, world: int, merged: bool = False) -> List[List[int]]:
+    """Each rank's edges (ascending) under the library's LPT placement."""
+    own = q.shard_edges(g, p, world, merged=merged)
+    return [sorted(int(i) for i in np.nonzero(own == r)[0]) for r in range(max(1, world))]
 
 
 def shard_imbalance(costs: Sequence[float], shards: List[List[int]]) -> float:

@@ -24,6 +24,12 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def golden_merged():
+    with open(os.path.join(GOLDEN, "merged.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
 def golden_buckets():
     with open(os.path.join(GOLDEN, "buckets.json")) as f:
         return json.load(f)

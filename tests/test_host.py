@@ -150,3 +150,64 @@ def test_edge_work_is_the_reference_op_count(q, golden):
     ops = q.plan_stats(g, 4).sum_ops
     assert w.sum() >= ops
     assert w.argmax() == q.edge_costs(g, 4).argmax()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
+def test_merged_schedules_match_reference(q, golden_merged, name):
+    """merge_buckets (engine.cpp:306-358): every edge's merged schedule --
+    bucket order, sum vars, member order -- its simulated widths and its
+    merges_applied/merges_skipped counters equal the reference's
+    (tests/golden/merged.json, oracle/gen_golden_merged.py)."""
+    c = golden_merged[name]
+    g = q.random_regular(c["n"], 3, c["seed"])
+    a = q.Angles(c["gammas"], c["betas"])
+    fp_b, fp_w, applied, skipped = [], [], [], []
+    for i in range(g.m):
+        s = q.edge_schedule(g, i, a, merged=True)
+        for b in s.buckets:
+            fp_b += b.sum_vars + [-2]
+            for t in b.tensors:
+                fp_b += t.vars + [-3]
+            fp_b += [-4]
+        fp_b.append(-1)
+        fp_w += q.simulate_widths(g, i, a.depth(), merged=True) + [-5]
+        applied.append(s.merges_applied)
+        skipped.append(s.merges_skipped)
+    assert "%016x" % O.fnv1a_int64(fp_b) == c["merged_buckets"]
+    assert "%016x" % O.fnv1a_int64(fp_w) == c["merged_widths"]
+    assert applied == c["merges_applied"]
+    assert skipped == c["merges_skipped"]
+
+
+def test_merged_schedules_live_reference(q, golden):
+    """Merged C1 and a handful of C2 edges against the live reference build."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    for name, sel in (("C1", None), ("C2", [0, 7, 22, 31, 44])):
+        c = golden["configs"][name]
+        g = q.random_regular(c["n"], 3, c["seed"])
+        a = q.Angles(c["gammas"], c["betas"])
+        for i in (range(g.m) if sel is None else sel):
+            ints, data, nb = O.ref_edge_schedule(c["n"], g.edges, c["gammas"], c["betas"], i,
+                                                 merged=True)
+            s = q.edge_schedule(g, i, a, merged=True)
+            mi, mn, md = s.flatten()
+            assert np.array_equal(mi[:mn], ints) and np.array_equal(md, data), (name, i)
+            assert (s.merges_applied, s.merges_skipped) == O.ref_merge_counts(
+                c["n"], g.edges, c["gammas"], c["betas"], i)
+
+
+def test_lpt_shards_on_predicted_work(q, golden):
+    """qtng_shard_edges: LPT placement of the lightcones by predicted work --
+    every edge placed once, loads within LPT's bound, deterministic."""
+    c = golden["configs"]["C2"]
+    g = q.random_regular(c["n"], 3, c["seed"])
+    w = q.edge_work(g, 4)
+    for k in (1, 2, 4, 8):
+        own = q.shard_edges(g, 4, k)
+        assert own.shape == (g.m,) and own.min() >= 0 and own.max() < k
+        loads = np.array([w[own == r].sum() for r in range(k)])
+        # LPT: max load <= mean + the largest single job
+        assert loads.max() <= loads.mean() + w.max() + 1e-6
+        assert np.array_equal(own, q.shard_edges(g, 4, k))
+    assert (q.shard_edges(g, 4, 1) == 0).all()
