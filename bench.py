@@ -478,9 +478,10 @@ def sub_c4(q, ctx, args, steps=10):
     plan.run_device(3)
     dev_ms = plan.run_device(steps) / steps
     replay_terms = plan.terms()
-    e = 0.5 * g.m
+    acc = 0.0  # engine.cpp:549-551: sum in edge order, then m/2 - sum/2
     for x in replay_terms.real:
-        e -= 0.5 * float(x)
+        acc += float(x)
+    e = 0.5 * g.m - 0.5 * acc
     for _ in range(2):
         q.energy_expectation(g, a, q.GpuBackend(ctx))
     torch.cuda.synchronize()
@@ -514,9 +515,10 @@ def sub_c64(q, ctx, cfg, args, steps=10):
     plan.run_device(3)
     dev_ms = plan.run_device(steps) / steps
     t = plan.terms()
-    e = 0.5 * g.m
+    acc = 0.0
     for x in t.real:
-        e -= 0.5 * float(x)
+        acc += float(x)
+    e = 0.5 * g.m - 0.5 * acc
     gold = golden_energy("C2")
     plan.close()
     return {"value": g.m / (dev_ms / 1e3), "unit": "lightcones/s", "ms_per_step": dev_ms,
