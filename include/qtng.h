@@ -244,10 +244,17 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
 qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* ints,
                                       int64_t n_ints, const double* data, int max_result_width,
                                       qtng_plan** out);
-/* Run the plan for one angle set.  terms (host, may be NULL) receives
- * 2*n_sel doubles.  device_ms (may be NULL) = device time of the kernels
- * (CUDA events on the plan's stream). */
+/* Run the plan for one angle set: ONE CUDA-graph launch holding the
+ * gate-table upload (memcpy node from the plan's pinned staging), every
+ * level's kernels and the terms download.  terms (host, may be NULL)
+ * receives 2*n_sel doubles.  device_ms (may be NULL) = device time of the
+ * graph (CUDA events on the plan's stream). */
 qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const double* betas,
+                              double* terms, float* device_ms);
+/* qtng_plan_execute enqueued eagerly with CUDA events around every level and
+ * every kernel (the measurement behind qtng_plan_level_ms / _kernel_ms and
+ * the per-level record times); same results. */
+qtng_status qtng_plan_profile(qtng_plan* plan, const double* gammas, const double* betas,
                               double* terms, float* device_ms);
 /* Device-only re-execution with the current angles (no host copies), for
  * throughput measurement: the plan captured once as a CUDA graph, n_runs
@@ -274,7 +281,8 @@ qtng_status qtng_statevector_energy(qtng_ctx* ctx, int n, int m, const int* edge
 
 /* Host-only analysis of the fused-chain segments of the plan for all m
  * edges.  Per segment (level-sorted): level, L (stages), rY, cY, nops, rb
- * (paired rows: the tile bit of the second row, 255 = unpaired); then
+ * (paired rows: the tile bit of the second row, 255 = unpaired), rb2 (quad
+ * tiles: B's row bit, rb = A's; 255 = not quad); then
  * per stage: nt, ns, main (-1 for stage 1), and per member: rank,
  * initial (1 = gate / input-region tensor; a main placeholder has rank 0),
  * then its rank axis codes (device_plan.hpp: lane / digit / tile / summed bit).
@@ -285,15 +293,18 @@ qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged
  * fused-chain segments, fuse=0: one device op per bucket), without a device. */
 qtng_status qtng_plan_stats(int n, int m, const int* edges, int p, int merged,
                             int max_result_width, int fuse, qtng_plan_info* info);
-/* Records of the last execution (edge_u/edge_v filled from the selection). */
+/* Records of the last execution (edge_u/edge_v filled from the selection);
+ * elapsed_s = the bucket's byte share of its level's time after
+ * qtng_plan_profile, else of the last run's total device time. */
 qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64_t cap,
                               int64_t* n_out);
-/* Device time of the last qtng_plan_execute summed per kernel kind (ms):
- * ms3[0] level_kernel, ms3[1] outer_kernel, ms3[2] seg_kernel -- CUDA events
- * on the stream each kernel runs on.  per_level (optional, cap entries):
- * the same three times for each level, level-major. */
-qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3, float* per_level, int cap);
-/* Per-level device time of the last qtng_plan_execute (ms), n_levels entries. */
+/* Device time of the last qtng_plan_profile summed per kernel kind (ms):
+ * ms4[0] level_kernel, ms4[1] outer_kernel, ms4[2] seg_kernel, ms4[3]
+ * seg4_kernel (quad tiles) -- CUDA events on the stream each kernel runs on.
+ * per_level (optional, cap entries): the same four times for each level,
+ * level-major. */
+qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms4, float* per_level, int cap);
+/* Per-level device time of the last qtng_plan_profile (ms), n_levels entries. */
 qtng_status qtng_plan_level_ms(const qtng_plan* plan, float* ms, int cap);
 void qtng_plan_destroy(qtng_plan* plan);
 

@@ -487,7 +487,8 @@ def plan_stats(g: Graph, p: int, merged: bool = False, cfg: Optional[EngineConfi
 def plan_segments(g: Graph, p: int, merged: bool = False,
                   cfg: Optional[EngineConfig] = None) -> List[dict]:
     """Host-only description of the fused-chain segments of Plan(g, p):
-    level, L, ry, cy, nops, rb (paired rows' tile bit or None),
+    level, L, ry, cy, nops, rb (paired rows' tile bit or None), rb2 (quad tiles:
+    B's row bit, rb = A's; None otherwise),
     stages=[(nt, ns, main, [(rank, initial, codes)])]."""
     cfg = cfg or EngineConfig()
     n_ints = C.c_int64(0)
@@ -499,8 +500,8 @@ def plan_segments(g: Graph, p: int, merged: bool = False,
                                   buf, len(buf), C.byref(n_ints)))
     out, i = [], 0
     while i < n_ints.value:
-        lv, L, ry, cy, nops, rb = (int(x) for x in buf[i:i + 6])
-        i += 6
+        lv, L, ry, cy, nops, rb, rb2 = (int(x) for x in buf[i:i + 7])
+        i += 7
         stages = []
         for _ in range(L):
             nt, ns, main = (int(x) for x in buf[i:i + 3])
@@ -512,7 +513,8 @@ def plan_segments(g: Graph, p: int, merged: bool = False,
                 i += 2 + rank
             stages.append((nt, ns, main, mem))
         out.append(dict(level=lv, L=L, ry=ry, cy=cy, nops=nops,
-                        rb=None if rb == 0xff else rb, stages=stages))
+                        rb=None if rb == 0xff else rb, rb2=None if rb2 == 0xff else rb2,
+                        stages=stages))
     return out
 
 
@@ -683,7 +685,16 @@ class Plan:
         return self
 
     def execute(self, angles: Optional[Angles] = None) -> np.ndarray:
-        """Per-edge complex e_jk of the selected edges (selection order)."""
+        """Per-edge complex e_jk of the selected edges (selection order): one
+        CUDA-graph launch (gate-table upload + kernels + terms download)."""
+        return self._run(lib.qtng_plan_execute, angles)
+
+    def profile(self, angles: Optional[Angles] = None) -> np.ndarray:
+        """execute() enqueued eagerly with CUDA events around every level and
+        kernel; fills level_ms(), kernel_ms(), level_kernel_ms()."""
+        return self._run(lib.qtng_plan_profile, angles)
+
+    def _run(self, fn, angles) -> np.ndarray:
         if self.p:
             gam, bet = _angles_arrays(angles)
             if len(gam) != self.p or len(bet) != self.p:
@@ -693,8 +704,7 @@ class Plan:
             gp = bp = None
         out = np.zeros(2 * max(1, len(self.sel)), np.float64)
         ms = C.c_float(0)
-        _check(lib.qtng_plan_execute(self._h, gp, bp, out.ctypes.data_as(C.c_void_p),
-                                     C.byref(ms)))
+        _check(fn(self._h, gp, bp, out.ctypes.data_as(C.c_void_p), C.byref(ms)))
         self.last_device_ms = ms.value
         return out[: 2 * len(self.sel)].view(np.complex128).copy()
 
@@ -718,17 +728,18 @@ class Plan:
         return out[:n]
 
     def kernel_ms(self) -> dict:
-        """Device ms of the last execute() per kernel kind (events on each kernel's stream)."""
-        ms = np.zeros(3, np.float32)
+        """Device ms of the last profile() per kernel kind (events on each kernel's stream)."""
+        ms = np.zeros(4, np.float32)
         _check(lib.qtng_plan_kernel_ms(self._h, ms, None, 0))
-        return {"level_kernel": float(ms[0]), "outer_kernel": float(ms[1]), "seg_kernel": float(ms[2])}
+        return {"level_kernel": float(ms[0]), "outer_kernel": float(ms[1]), "seg_kernel": float(ms[2]),
+                "seg4_kernel": float(ms[3])}
 
     def level_kernel_ms(self) -> np.ndarray:
-        """(n_levels, 3) device ms of the last execute(): level / outer / seg kernel per level."""
+        """(n_levels, 4) device ms of the last profile(): level / outer / seg / seg4 kernel per level."""
         n = self.info().n_levels
-        ms, per = np.zeros(3, np.float32), np.zeros(3 * max(1, n), np.float32)
-        _check(lib.qtng_plan_kernel_ms(self._h, ms, per.ctypes.data_as(C.c_void_p), 3 * n))
-        return per[:3 * n].reshape(n, 3)
+        ms, per = np.zeros(4, np.float32), np.zeros(4 * max(1, n), np.float32)
+        _check(lib.qtng_plan_kernel_ms(self._h, ms, per.ctypes.data_as(C.c_void_p), 4 * n))
+        return per[:4 * n].reshape(n, 4)
 
     def time_level(self, level: int = -1, n_runs: int = 10):
         lv, by, ms = C.c_int(0), C.c_double(0), C.c_float(0)

@@ -218,7 +218,7 @@ DescLayout layout_of(const HostPlan& hp) {
   L.segs = o; o = align256(o + hp.segs.size() * sizeof(DevSeg));
   L.seg_ibeg = o; o = align256(o + hp.seg_ibeg.size() * sizeof(uint32_t));
   L.stages = o; o = align256(o + hp.stages.size() * sizeof(DevStage));
-  L.ctr = o; o = align256(o + hp.levels.size() * 2 * sizeof(uint32_t));
+  L.ctr = o; o = align256(o + hp.levels.size() * 4 * sizeof(uint32_t));
   L.scal = o; o = align256(o + hp.scalar_off.size() * sizeof(uint64_t));
   L.lcb = o; o = align256(o + hp.lc_begin.size() * sizeof(uint32_t));
   L.lce = o; o = align256(o + hp.lc_edge.size() * sizeof(int32_t));
@@ -243,7 +243,7 @@ void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
   std::memcpy(dst + L.segs, hp.segs.data(), hp.segs.size() * sizeof(DevSeg));
   std::memcpy(dst + L.seg_ibeg, hp.seg_ibeg.data(), hp.seg_ibeg.size() * sizeof(uint32_t));
   std::memcpy(dst + L.stages, hp.stages.data(), hp.stages.size() * sizeof(DevStage));
-  std::memset(dst + L.ctr, 0, hp.levels.size() * 2 * sizeof(uint32_t));  // seg_kernel work counters
+  std::memset(dst + L.ctr, 0, hp.levels.size() * 4 * sizeof(uint32_t));  // seg(4)_kernel work counters
   std::memcpy(dst + L.funits, hp.flow_units.data(), hp.flow_units.size() * sizeof(FlowUnit));
   std::memcpy(dst + L.finit, hp.flow_init.data(), hp.flow_init.size() * sizeof(uint64_t));
   std::memcpy(dst + L.scal, hp.scalar_off.data(), hp.scalar_off.size() * sizeof(uint64_t));
@@ -261,6 +261,8 @@ void pack_desc(const HostPlan& hp, const DescLayout& L, char* dst) {
 struct Lane {
   cudaStream_t s = nullptr, s2 = nullptr, s3 = nullptr;
   cudaEvent_t fork = nullptr, join2 = nullptr, join3 = nullptr;
+  cudaStream_t s4 = nullptr;      // quad-tile segment kernels, forked per level
+  cudaEvent_t join4 = nullptr;
   DevBuf* arena = nullptr;
   DevBuf* desc = nullptr;
   PinBuf *pin_desc = nullptr, *pin_in = nullptr, *pin_out = nullptr;
@@ -320,7 +322,8 @@ struct DevProgram {
   SegOpTab* segtab() const { return reinterpret_cast<SegOpTab*>(base + L.segtab); }
   template <class T>
   T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
-  uint32_t* ctr(size_t level) const { return reinterpret_cast<uint32_t*>(base + L.ctr) + 2 * level; }
+  // per level: seg_kernel's tile queue (2 counters), then seg4_kernel's
+  uint32_t* ctr(size_t level) const { return reinterpret_cast<uint32_t*>(base + L.ctr) + 4 * level; }
   const uint64_t* scal() const { return reinterpret_cast<const uint64_t*>(base + L.scal); }
   const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
   const int32_t* lce() const { return reinterpret_cast<const int32_t*>(base + L.lce); }
@@ -329,18 +332,29 @@ struct DevProgram {
 
 // One level: the outer-join and segment kernels forked onto side streams, the
 // generic kernel on the main stream, joined before the next level.
-// kev (optional): 6 events bracketing this level's level / outer / segment
-// kernels on the streams they run on (per-kernel device time).
+// kev (optional): 8 events bracketing this level's level / outer / segment /
+// quad-segment kernels on the streams they run on (per-kernel device time).
 void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const DevProgram& pr,
                    void* arena, cudaEvent_t* kev = nullptr, const Lane* ln = nullptr) {
   const Lane& la = ln ? *ln : ctx->lane[0];
   const bool c64 = pr.c64;
   const bool fork2 = lv.outer_items > 0;
-  const bool fork3 = lv.seg_items > 0 && (lv.items > 0 || fork2);
+  const bool fork3 = lv.seg_items > 0 && (lv.items > 0 || fork2 || lv.seg4_items > 0);
+  const bool fork4 = lv.seg4_items > 0;
   auto rec = [&](int k, cudaStream_t st) {
     if (kev) QTNG_CUDA(cudaEventRecord(kev[k], st));
   };
-  if (fork2 || fork3) QTNG_CUDA(cudaEventRecord(la.fork, la.s));
+  if (fork2 || fork3 || fork4) QTNG_CUDA(cudaEventRecord(la.fork, la.s));
+  if (fork4) {  // quad-tile segments first: they are the level's longest kernel
+    QTNG_CUDA(cudaStreamWaitEvent(la.s4, la.fork, 0));
+    rec(6, la.s4);
+    QTNG_CUDA(c64 ? c64::launch_segs4(la.s4, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
+                                      pr.segtab(), arena, pr.ctr(level) + 2, lv)
+                  : c128::launch_segs4(la.s4, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
+                                       pr.segtab(), arena, pr.ctr(level) + 2, lv));
+    rec(7, la.s4);
+    QTNG_CUDA(cudaEventRecord(la.join4, la.s4));
+  }
   if (fork2) {
     QTNG_CUDA(cudaStreamWaitEvent(la.s2, la.fork, 0));
     rec(2, la.s2);
@@ -364,6 +378,7 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
   rec(1, la.s);
   if (fork2) QTNG_CUDA(cudaStreamWaitEvent(la.s, la.join2, 0));
   if (fork3) QTNG_CUDA(cudaStreamWaitEvent(la.s, la.join3, 0));
+  if (fork4) QTNG_CUDA(cudaStreamWaitEvent(la.s, la.join4, 0));
 }
 
 size_t elem_bytes(const HostPlan& hp) { return hp.c64 ? sizeof(float2) : sizeof(double2); }
@@ -425,7 +440,7 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, vo
   for (size_t L = 0; L < hp.levels.size() && !hp.flow; ++L) {
     if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[L], s));
     enqueue_level(ctx, hp.levels[L], L, pr, arena,
-                  kernel_events ? kernel_events->data() + 6 * L : nullptr, &la);
+                  kernel_events ? kernel_events->data() + 8 * L : nullptr, &la);
   }
   if (level_events) QTNG_CUDA(cudaEventRecord((*level_events)[hp.levels.size()], s));
   QTNG_CUDA((pr.c64 ? c64::launch_final : c128::launch_final)(
@@ -435,13 +450,14 @@ void enqueue_program(qtng_ctx* ctx, const HostPlan& hp, const DevProgram& pr, vo
 
 int launches_per_run(const HostPlan& hp) {
   if (hp.flow) return 3;  // flow_reset, flow_kernel, final_kernel
-  int lv = 0, outer = 0, seg = 0;
+  int lv = 0, outer = 0, seg = 0, seg4 = 0;
   for (const LevelLaunch& l : hp.levels) {
     lv += l.items > 0;
     outer += l.outer_items > 0;
     seg += l.seg_items > 0;
+    seg4 += l.seg4_items > 0;
   }
-  return kernels_per_plan(lv, outer, seg);
+  return kernels_per_plan(lv, outer, seg, seg4);
 }
 
 // Ops of the reference's run_edge post-processing (engine.cpp:517-519, 543-546).
@@ -481,15 +497,20 @@ struct qtng_plan {
   PinBuf pin_gate, pin_terms;
   std::vector<cudaEvent_t> lev_ev;
   std::vector<float> level_ms;
-  std::vector<cudaEvent_t> ker_ev;  // 6 per level (enqueue_level)
-  float kernel_ms[3] = {0.f, 0.f, 0.f};  // level / outer / segment kernels, last execute
-  std::vector<float> level_kernel_ms;    // 3 per level, last execute
-  cudaGraphExec_t graph = nullptr;
+  std::vector<cudaEvent_t> ker_ev;  // 8 per level (enqueue_level)
+  float kernel_ms[4] = {0.f, 0.f, 0.f, 0.f};  // level / outer / seg / seg4 kernels, last profile
+  std::vector<float> level_kernel_ms;    // 4 per level, last profile
+  cudaGraphExec_t graph = nullptr;       // kernels only (qtng_plan_run_device)
   uint64_t graph_gen = ~uint64_t{0};
+  cudaGraphExec_t graph_io = nullptr;    // gate-table H2D + kernels + terms D2H (qtng_plan_execute)
+  uint64_t graph_io_gen = ~uint64_t{0};
+  float last_ms = 0.f;                   // device time of the last execute / run
+  bool profiled = false;                 // level_ms holds a qtng_plan_profile measurement
   ~qtng_plan() {
     for (cudaEvent_t e : lev_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : ker_ev) cudaEventDestroy(e);
     if (graph) cudaGraphExecDestroy(graph);
+    if (graph_io) cudaGraphExecDestroy(graph_io);
   }
 };
 
@@ -518,10 +539,23 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
     QTNG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     QTNG_CUDA(cudaEventCreateWithFlags(&ctx->join3_ev, cudaEventDisableTiming));
     Lane& l0 = ctx->lane[0];
-    l0 = Lane{ctx->stream, ctx->stream2, ctx->stream3, ctx->fork_ev, ctx->join_ev, ctx->join3_ev,
-              &ctx->arena, &ctx->desc, &ctx->pin_desc, &ctx->pin_in, &ctx->pin_out};
-    for (int i = 0; i < qtng_ctx::kLanes; ++i)
+    l0 = Lane{};
+    l0.s = ctx->stream;
+    l0.s2 = ctx->stream2;
+    l0.s3 = ctx->stream3;
+    l0.fork = ctx->fork_ev;
+    l0.join2 = ctx->join_ev;
+    l0.join3 = ctx->join3_ev;
+    l0.arena = &ctx->arena;
+    l0.desc = &ctx->desc;
+    l0.pin_desc = &ctx->pin_desc;
+    l0.pin_in = &ctx->pin_in;
+    l0.pin_out = &ctx->pin_out;
+    for (int i = 0; i < qtng_ctx::kLanes; ++i) {
       for (cudaEvent_t* ev : {&ctx->lane[i].t0, &ctx->lane[i].t1}) QTNG_CUDA(cudaEventCreate(ev));
+      QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->lane[i].s4, cudaStreamNonBlocking));
+      QTNG_CUDA(cudaEventCreateWithFlags(&ctx->lane[i].join4, cudaEventDisableTiming));
+    }
     for (int i = 1; i < qtng_ctx::kLanes; ++i) {
       Lane& l1 = ctx->lane[i];
       l1.arena = &ctx->arena_x[i];
@@ -556,9 +590,14 @@ void qtng_destroy(qtng_ctx* ctx) {
     for (cudaEvent_t e : {l1.fork, l1.join2, l1.join3})
       if (e) cudaEventDestroy(e);
   }
-  for (int i = 0; i < qtng_ctx::kLanes; ++i)
-    for (cudaEvent_t e : {ctx->lane[i].t0, ctx->lane[i].t1})
+  for (int i = 0; i < qtng_ctx::kLanes; ++i) {
+    if (ctx->lane[i].s4) {
+      cudaStreamSynchronize(ctx->lane[i].s4);
+      streams.push_back(ctx->lane[i].s4);
+    }
+    for (cudaEvent_t e : {ctx->lane[i].t0, ctx->lane[i].t1, ctx->lane[i].join4})
       if (e) cudaEventDestroy(e);
+  }
   for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev})
     if (e) cudaEventDestroy(e);
   delete ctx;  // frees the arenas and staging buffers
@@ -867,7 +906,7 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
     plan->pin_terms.ensure(std::max<size_t>(1, cs.walks.size()) * sizeof(double2));
     plan->lev_ev.resize(hp.levels.size() + 1);
     for (cudaEvent_t& e : plan->lev_ev) QTNG_CUDA(cudaEventCreate(&e));
-    plan->ker_ev.resize(6 * hp.levels.size());
+    plan->ker_ev.resize(8 * hp.levels.size());
     for (cudaEvent_t& e : plan->ker_ev) QTNG_CUDA(cudaEventCreate(&e));
     plan->level_ms.assign(hp.levels.size(), 0.f);
     *out = plan.release();
@@ -905,12 +944,50 @@ qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* i
     plan->pin_terms.ensure(sizeof(double2));
     plan->lev_ev.resize(hp.levels.size() + 1);
     for (cudaEvent_t& e : plan->lev_ev) QTNG_CUDA(cudaEventCreate(&e));
-    plan->ker_ev.resize(6 * hp.levels.size());
+    plan->ker_ev.resize(8 * hp.levels.size());
     for (cudaEvent_t& e : plan->ker_ev) QTNG_CUDA(cudaEventCreate(&e));
     plan->level_ms.assign(hp.levels.size(), 0.f);
     *out = plan.release();
   });
 }
+
+}  // extern "C"
+
+namespace {
+
+// Fill the plan's pinned input staging for one angle set (QAOA plans: the
+// gate table; explicit schedules keep the data given at creation).
+void stage_plan_inputs(qtng_plan* plan, const double* gammas, const double* betas) {
+  const HostPlan& hp = plan->hp;
+  if (plan->explicit_sched) return;
+  std::vector<double> table(2 * hp.input_elems);
+  fill_gate_table(plan->p, gammas, betas, table.data());
+  stage_input(hp, table.data(), hp.input_elems, plan->pin_gate.p);
+}
+
+// Capture `body` on the context stream into an executable graph.
+template <class F>
+cudaGraphExec_t capture(qtng_ctx* ctx, F&& body) {
+  cudaGraph_t gr = nullptr;
+  QTNG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaStreamEndCapture(ctx->stream, &gr);
+    if (gr) cudaGraphDestroy(gr);
+    throw;
+  }
+  QTNG_CUDA(cudaStreamEndCapture(ctx->stream, &gr));
+  cudaGraphExec_t ex = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&ex, gr, 0);
+  cudaGraphDestroy(gr);
+  QTNG_CUDA(e);
+  return ex;
+}
+
+}  // namespace
+
+extern "C" {
 
 qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const double* betas,
                               double* terms, float* device_ms) {
@@ -922,11 +999,49 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     ctx->ensure_arena(hp.arena_elems, elem_bytes(hp));
-    if (!plan->explicit_sched) {
-      std::vector<double> table(2 * hp.input_elems);
-      fill_gate_table(plan->p, gammas, betas, table.data());
-      stage_input(hp, table.data(), hp.input_elems, plan->pin_gate.p);
+    stage_plan_inputs(plan, gammas, betas);
+    const size_t nb = plan->edges.size() * sizeof(double2);
+    // one graph: the gate-table upload (memcpy node from the plan's pinned
+    // staging), every level's kernels, the terms download -- re-captured only
+    // when the context's arena moves
+    if (!plan->graph_io || plan->graph_io_gen != ctx->arena_gen) {
+      if (plan->graph_io) cudaGraphExecDestroy(plan->graph_io);
+      plan->graph_io = nullptr;
+      plan->graph_io = capture(ctx, [&] {
+        QTNG_CUDA(cudaMemcpyAsync(ctx->arena.p, plan->pin_gate.p, hp.input_elems * elem_bytes(hp),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+        enqueue_program(ctx, hp, plan->prog, ctx->arena.p, nullptr);
+        QTNG_CUDA(cudaMemcpyAsync(plan->pin_terms.p, plan->prog.terms(), nb,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+      });
+      plan->graph_io_gen = ctx->arena_gen;
     }
+    QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    QTNG_CUDA(cudaGraphLaunch(plan->graph_io, ctx->stream));
+    QTNG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    g_launches.fetch_add(static_cast<uint64_t>(launches_per_run(hp)), std::memory_order_relaxed);
+    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    QTNG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    plan->last_ms = ms;
+    if (device_ms) *device_ms = ms;
+    const double* t = static_cast<const double*>(plan->pin_terms.p);
+    if (terms) std::memcpy(terms, t, nb);
+    if (!plan->explicit_sched) check_terms(plan->edges, t, imag_tol(hp.c64));
+  });
+}
+
+qtng_status qtng_plan_profile(qtng_plan* plan, const double* gammas, const double* betas,
+                              double* terms, float* device_ms) {
+  return guarded([&] {
+    if (!plan) throw Error(kInvalidInput, "null plan");
+    if (!plan->explicit_sched) validate_angles(plan->p, gammas, betas);
+    qtng_ctx* ctx = plan->ctx;
+    const HostPlan& hp = plan->hp;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QTNG_CUDA(cudaSetDevice(ctx->device));
+    ctx->ensure_arena(hp.arena_elems, elem_bytes(hp));
+    stage_plan_inputs(plan, gammas, betas);
     QTNG_CUDA(cudaMemcpyAsync(ctx->arena.p, plan->pin_gate.p, hp.input_elems * elem_bytes(hp),
                               cudaMemcpyHostToDevice, ctx->stream));
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -941,19 +1056,21 @@ qtng_status qtng_plan_execute(qtng_plan* plan, const double* gammas, const doubl
     for (size_t L = 0; L < hp.levels.size(); ++L)
       QTNG_CUDA(cudaEventElapsedTime(&plan->level_ms[L], plan->lev_ev[L], plan->lev_ev[L + 1]));
     for (float& k : plan->kernel_ms) k = 0.f;
-    plan->level_kernel_ms.assign(3 * hp.levels.size(), 0.f);
+    plan->level_kernel_ms.assign(4 * hp.levels.size(), 0.f);
     if (hp.flow) plan->kernel_ms[2] = plan->level_ms.empty() ? 0.f : plan->level_ms[0];
     for (size_t L = 0; L < hp.levels.size() && !hp.flow; ++L) {
       const LevelLaunch& lv = hp.levels[L];
-      const uint32_t present[3] = {lv.items, lv.outer_items, lv.seg_items};
-      for (int k = 0; k < 3; ++k) {
+      const uint32_t present[4] = {lv.items, lv.outer_items, lv.seg_items, lv.seg4_items};
+      for (int k = 0; k < 4; ++k) {
         if (!present[k]) continue;
-        float ms = 0.f;
-        QTNG_CUDA(cudaEventElapsedTime(&ms, plan->ker_ev[6 * L + 2 * k], plan->ker_ev[6 * L + 2 * k + 1]));
-        plan->kernel_ms[k] += ms;
-        plan->level_kernel_ms[3 * L + k] = ms;
+        float kms = 0.f;
+        QTNG_CUDA(cudaEventElapsedTime(&kms, plan->ker_ev[8 * L + 2 * k], plan->ker_ev[8 * L + 2 * k + 1]));
+        plan->kernel_ms[k] += kms;
+        plan->level_kernel_ms[4 * L + k] = kms;
       }
     }
+    plan->last_ms = ms;
+    plan->profiled = true;
     if (device_ms) *device_ms = ms;
     const double* t = static_cast<const double*>(plan->pin_terms.p);
     if (terms) std::memcpy(terms, t, nb);
@@ -972,12 +1089,7 @@ qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms) 
     if (!plan->graph || plan->graph_gen != ctx->arena_gen) {
       if (plan->graph) cudaGraphExecDestroy(plan->graph);
       plan->graph = nullptr;
-      cudaGraph_t gr = nullptr;
-      QTNG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      enqueue_program(ctx, hp, plan->prog, ctx->arena.p, nullptr);
-      QTNG_CUDA(cudaStreamEndCapture(ctx->stream, &gr));
-      QTNG_CUDA(cudaGraphInstantiate(&plan->graph, gr, 0));
-      cudaGraphDestroy(gr);
+      plan->graph = capture(ctx, [&] { enqueue_program(ctx, hp, plan->prog, ctx->arena.p, nullptr); });
       plan->graph_gen = ctx->arena_gen;
     }
     QTNG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -988,6 +1100,7 @@ qtng_status qtng_plan_run_device(qtng_plan* plan, int n_runs, float* device_ms) 
     QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;
     QTNG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    plan->last_ms = ms / std::max(1, n_runs);
     if (device_ms) *device_ms = ms;
   });
 }
@@ -1035,9 +1148,9 @@ qtng_status qtng_plan_segments(int n, int m, const int* edges, int p, int merged
     const HostPlan hp = build_plan(ptrs, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, true, true);
     std::vector<int> out;
     for (size_t L = 0; L < hp.levels.size(); ++L)
-      for (uint32_t k = 0; k < hp.levels[L].seg_count; ++k) {
+      for (uint32_t k = 0; k < hp.levels[L].seg_count + hp.levels[L].seg4_count; ++k) {
         const DevSeg& sg = hp.segs[hp.levels[L].seg_begin + k];
-        out.insert(out.end(), {static_cast<int>(L), sg.nst, sg.ry, sg.cy, sg.nops, sg.rb});
+        out.insert(out.end(), {static_cast<int>(L), sg.nst, sg.ry, sg.cy, sg.nops, sg.rb, sg.rb2});
         for (int i = 0; i < sg.nst; ++i) {
           const DevStage& st = hp.stages[sg.stage + i];
           out.insert(out.end(), {st.nt, st.ns, st.main == kSegMain ? -1 : st.main});
@@ -1139,17 +1252,24 @@ qtng_status qtng_plan_records(const qtng_plan* plan, qtng_record* records, int64
         r.width = hp.rec_width[i];
         r.ops = uint64_t{1} << r.width;
         const int L = hp.rec_level[i];
-        const double share = hp.level_bytes[L] > 0 ? hp.rec_bytes[i] / hp.level_bytes[L] : 0;
-        r.elapsed_s = std::max(1e-9, 1e-3 * plan->level_ms[L] * share);
+        double share, ms;
+        if (plan->profiled) {  // the bucket's byte share of its level's measured time
+          share = hp.level_bytes[L] > 0 ? hp.rec_bytes[i] / hp.level_bytes[L] : 0;
+          ms = plan->level_ms[L];
+        } else {  // ... of the whole program's (graph replay)
+          share = hp.alg_bytes > 0 ? hp.rec_bytes[i] / hp.alg_bytes : 0;
+          ms = plan->last_ms;
+        }
+        r.elapsed_s = std::max(1e-9, 1e-3 * ms * share);
         r.flops_est = 8.0 * static_cast<double>(r.ops) / r.elapsed_s;
       }
   });
 }
 
-qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms3, float* per_level, int cap) {
+qtng_status qtng_plan_kernel_ms(const qtng_plan* plan, float* ms4, float* per_level, int cap) {
   return guarded([&] {
-    if (!plan || !ms3) throw Error(kInvalidInput, "null argument");
-    for (int k = 0; k < 3; ++k) ms3[k] = plan->kernel_ms[k];
+    if (!plan || !ms4) throw Error(kInvalidInput, "null argument");
+    for (int k = 0; k < 4; ++k) ms4[k] = plan->kernel_ms[k];
     if (per_level)
       for (int i = 0; i < cap && i < static_cast<int>(plan->level_kernel_ms.size()); ++i)
         per_level[i] = plan->level_kernel_ms[i];

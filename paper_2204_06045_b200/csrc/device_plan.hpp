@@ -88,10 +88,12 @@ constexpr int kSegMaxNt = 4;         // members of a fused stage (incl. the main
 #define QTNG_SEG_PAIR_MAXNT 4
 #endif
 constexpr int kSegPairMaxNt = QTNG_SEG_PAIR_MAXNT;  // paired rows only for stage-1 member counts up to this
+constexpr int kSegQuadMaxNt = 4;    // quad tiles: stage-1 member counts 2..4
 constexpr uint8_t kSegMain = 0xff;   // DevStage::main of stage 1 (no main)
 constexpr uint8_t kLaneSrcEnd = 5;
 constexpr uint8_t kJSrc = 8;
 constexpr uint8_t kTileSrc = 32;
+constexpr uint8_t kNoVar = 0xff;  // DevSeg::rb / rb2, DevStage::u: none
 
 struct alignas(16) DevSeg {
   uint64_t out;         // arena element offset of Y
@@ -108,13 +110,26 @@ struct alignas(16) DevSeg {
   // so the side products are the same for both rows.  kNoVar: unpaired.  A
   // paired segment has half as many work items (tiles with bit rb removed).
   uint8_t rb;
-  uint8_t pad[7];
+  // Quad tiles (seg4_kernel; cY = 5, stage 1 = [prefix..., A, B]): a lane
+  // computes four Y rows, tile bits rb (read by A, not by B or the prefix)
+  // and rb2 (read by B only) = 0/1, the outer product of two A rows and two
+  // B rows: 2 + 2 operand loads per summed value for 4 terms.  Side members
+  // may read rb / rb2 (their products are then formed per row).  kNoVar:
+  // not a quad segment.  A quad segment has a quarter as many work items.
+  uint8_t rb2;
+  uint8_t pad[6];
 };
 static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
 
 // Per-operand tables of a segment, built on the device once per plan upload
 // (seg_prep_kernel) from the DevTensor bit maps and read by seg_kernel through
 // the read-only path.  Indexed like the DevTensor array.
+// log2 of a segment's work items: its tiles, halved for paired rows and
+// quartered for quad tiles.
+inline int seg_item_bits(const DevSeg& sg) {
+  return sg.ry - sg.cy - (sg.rb2 != kNoVar ? 2 : (sg.rb != kNoVar ? 1 : 0));
+}
+
 struct alignas(16) SegOpTab {
   uint64_t off;                // arena element offset
   uint32_t sd;                 // stage 1: offset of its own summed bit
@@ -142,7 +157,6 @@ struct DevStage {
   uint8_t pad;
 };
 static_assert(sizeof(DevStage) == 8, "DevStage layout");
-constexpr uint8_t kNoVar = 0xff;
 
 // One level of the level-synchronous schedule: generic ops
 // [op_begin, op_begin+op_count) of the level-sorted op array (`items` warp
@@ -159,6 +173,10 @@ struct LevelLaunch {
   uint32_t seg_begin;  // fused-chain segments [seg_begin, seg_begin+seg_count)
   uint32_t seg_count;
   uint32_t seg_items;  // tiles
+  // quad-tile segments (seg4_kernel): [seg_begin+seg_count, +seg4_count),
+  // item_begin counted from 0 within that group
+  uint32_t seg4_count;
+  uint32_t seg4_items;
 };
 
 // ---------------------------------------------------------------- dataflow

@@ -948,10 +948,13 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
 // (stage, entry) folds the stage's side members at (s_i, u0, u1) = entry bits
 // (a tile-bit u takes this tile's value) exactly like chain_side.  Cold path:
 // kept out of line so the hot loop's registers are not spilled for it.
+// fa / fb (quad tiles): tile-bit codes that stay table index bits (the rows'
+// bits) instead of taking the tile's value; kNoVar otherwise.
 __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
                                               const DevTensor* __restrict__ trefs,
                                               const V* __restrict__ arena, uint32_t tile,
-                                              int lane) {
+                                              int lane, uint8_t fa = kNoVar,
+                                              uint8_t fb = kNoVar) {
   for (int base = 8; base < 8 * sg.nst; base += 32) {
     const int i = (base + lane) >> 3, e = (base + lane) & 7;
     if (i < sg.nst && cw.st[i].ptab) {
@@ -960,7 +963,7 @@ __device__ __noinline__ void chain_ptab_build(ChainWarp& cw, const DevSeg& sg,
       auto val = [&](uint8_t c) -> uint32_t {
         if (c == own) return e & 1;
         const int w = c == st.u[0] ? 0 : 1;
-        if (c >= kTileSrc && c < kSumSrc) return (tile >> (c - kTileSrc)) & 1u;
+        if (c >= kTileSrc && c < kSumSrc && c != fa && c != fb) return (tile >> (c - kTileSrc)) & 1u;
         return (e >> (1 + w)) & 1;
       };
       V p = mkv(0.0, 0.0);
@@ -997,7 +1000,8 @@ struct SegCursor {
 // table-index bits.
 __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const DevSeg* __restrict__ segs,
                                            int si, const DevStage* __restrict__ stages,
-                                           const SegOpTab* __restrict__ segtab, int lane) {
+                                           const SegOpTab* __restrict__ segtab, int lane,
+                                           bool quad = false) {
   sc.cur = si;
   sc.sg = segs[si];
   const DevSeg& sg = sc.sg;
@@ -1010,8 +1014,9 @@ __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const D
     for (int t = 0; real && t < st.nt - 1; ++t)
       real = __ldg(&segtab[sg.tref + st.op0 + t].kind) == kTensorRealScalar;
     cw.preal[lane] = real ? 1 : 0;
-    for (int w = 0; w < 2; ++w)
-      tile_dep |= st.ptab && st.u[w] >= kTileSrc && st.u[w] < kSumSrc;
+    for (int w = 0; w < 2; ++w)  // quad rows' bits are table index bits, not tile values
+      tile_dep |= st.ptab && st.u[w] >= kTileSrc && st.u[w] < kSumSrc &&
+                  !(quad && (st.u[w] == kTileSrc + sg.rb || st.u[w] == kTileSrc + sg.rb2));
     const uint32_t mode = st.nt <= 1 ? 0u : (QTNG_SEG_PTAB && st.ptab ? (real ? 2u : 1u) : 3u);
     uint32_t d = mode;
     for (int w = 0; w < 2; ++w)
@@ -1075,6 +1080,308 @@ __device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t 
     default: chain_tile_u<6, 1>(cw, tab, sg, arena, tile, lane); break;
   }
   __syncwarp();
+}
+
+// ---------------------------------------------------------------- quad tiles
+// seg4_kernel: segments whose head (stage 1) is an outer join
+// [prefix..., A, B] -- A reads tile bit rb and B does not, B reads rb2 and A
+// does not, the prefix (the |+> scale, small gates) reads neither.  A lane
+// evaluates four Y rows at once, r = (rb, rb2) in {0,1}^2: per digit
+// assignment and summed value it loads A at rb = 0/1 and B at rb2 = 0/1 and
+// forms the 2 x 2 outer product PA[rb] * B[rb2] with PA = prefix * A -- four
+// terms from four operand loads, where a lane of seg_kernel loads two (paired)
+// or one (unpaired) operand per term.  Register reuse is the lever: every
+// operand value reaching the register file costs the SM's 128 B/clk L1 data
+// path, which bounds seg_kernel before its FP64 pipe does (ncu:
+// l1tex__data_pipe_lsu_wavefronts 59% vs FP64 30%).
+// Each row sees exactly the unfused operation sequence: left fold in member
+// order ((prefix * A) * B), summed values ascending, the climb as in
+// chain_tile2; a side member that reads rb / rb2 is gathered (or looked up)
+// per row.
+struct ChainWarp4 {
+  ChainWarp b;                          // rows 0 / 1 park in b.acc / b.acc1
+  V acc2[kSegMaxStages - 2][32];        // ... rows 2 / 3
+  V acc3[kSegMaxStages - 2][32];
+  uint32_t da[kSegMaxOps], db[kSegMaxOps];  // per operand: offset of tile bit rb / rb2
+  // per stage: bits 0-7 = ptab index bit fed by rb, 8-15 = by rb2; bit 16 / 17:
+  // a gathered side member reads rb / rb2
+  uint32_t rdesc[kSegMaxStages];
+};
+
+// Quad extras of the segment just loaded by seg_switch.
+__device__ __forceinline__ void seg_switch4(ChainWarp4& cw, const DevSeg& sg,
+                                            const SegOpTab* __restrict__ tab, int lane) {
+  if (lane < sg.nops) {
+    cw.da[lane] = __ldg(&tab[lane].dtile[sg.rb]);
+    cw.db[lane] = __ldg(&tab[lane].dtile[sg.rb2]);
+  }
+  __syncwarp();
+  if (lane >= 1 && lane < sg.nst) {
+    const DevStage st = cw.b.st[lane];
+    const uint32_t mode = cw.b.sdesc[lane] & 3u;
+    const uint8_t ca = static_cast<uint8_t>(kTileSrc + sg.rb), cb = static_cast<uint8_t>(kTileSrc + sg.rb2);
+    uint32_t d = 0;
+    if (mode == 1u || mode == 2u) {
+      for (int w = 0; w < 2; ++w) {
+        if (st.u[w] == ca) d |= 2u << w;
+        if (st.u[w] == cb) d |= (2u << w) << 8;
+      }
+    } else if (mode == 3u) {
+      for (int t = 0; t + 1 < st.nt; ++t) {
+        if (cw.da[st.op0 + t]) d |= 1u << 16;
+        if (cw.db[st.op0 + t]) d |= 1u << 17;
+      }
+    }
+    cw.rdesc[lane] = d;
+  }
+  __syncwarp();
+}
+
+// chain_side for row r of a quad tile (side members reading rb / rb2; cold:
+// kept out of line).
+__device__ __forceinline__ V chain_side_row(const ChainWarp4& cw, const SegOpTab* __restrict__ tab,
+                                            const V* __restrict__ arena, int op0, int m,
+                                            uint32_t j, int lane, int r, bool* real) {
+  const uint32_t jl = j & 15u, jh = j >> 4;
+  V p = mkv(0.0, 0.0);
+  bool pr = false;
+#pragma unroll
+  for (int t = 0; t < kSegMaxNt - 1; ++t) {
+    if (t >= m) break;
+    const int op = op0 + t;
+    const SegOpTab* tb = tab + op;
+    const bool xr = __ldg(&tb->kind) == kTensorRealScalar;
+    const V x = xr ? mkv(__ldg(&(arena + __ldg(&tb->off))->x), 0.0)
+                   : ld(arena + __ldg(&tb->off) +
+                        (cw.b.toff[op] + __ldg(&tb->llane[lane]) + __ldg(&tb->dlo[jl]) +
+                         __ldg(&tb->dhi[jh]) + ((r & 1) ? cw.da[op] : 0u) +
+                         ((r & 2) ? cw.db[op] : 0u)));
+    if (t == 0) {
+      p = x;
+      pr = xr;
+    } else {
+      p = fmul(p, pr, x, xr);
+      pr = false;
+    }
+  }
+  *real = pr;
+  return p;
+}
+
+// Stage k + 2's term for the four rows: x[r] = P(j, row r) * x[r].
+__device__ __forceinline__ void chain_term4(const ChainWarp4& cw, const SegOpTab* __restrict__ tab,
+                                            const V* __restrict__ arena, const DevStage st, int k,
+                                            uint32_t j, V (&x)[4], int lane) {
+  const uint32_t d = cw.b.sdesc[k + 1];
+  const uint32_t mode = d & 3u;
+  if (mode == 0) return;
+  const uint32_t rd = cw.rdesc[k + 1];
+  if (mode != 3) {
+    const uint32_t idx = cw.b.slane[k][lane] | ((j >> k) & 1u) |
+                         (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
+                         (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
+    const uint32_t ma = rd & 0xffu, mb = (rd >> 8) & 0xffu;
+    if (!(ma | mb)) {
+      const V p = cw.b.ptab[k][idx];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) x[r] = mode == 2 ? rscale(p.x, x[r]) : cmul(p, x[r]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const V p = cw.b.ptab[k][idx | ((r & 1) ? ma : 0u) | ((r & 2) ? mb : 0u)];
+        x[r] = mode == 2 ? rscale(p.x, x[r]) : cmul(p, x[r]);
+      }
+    }
+    return;
+  }
+  if (!(rd >> 16)) {
+    bool real;
+    const V p = chain_side(cw.b, tab, arena, st.op0, st.nt - 1, j, lane, &real);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) x[r] = real ? rscale(p.x, x[r]) : cmul(p, x[r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      bool real;
+      const V p = chain_side_row(cw, tab, arena, st.op0, st.nt - 1, j, lane, r, &real);
+      x[r] = real ? rscale(p.x, x[r]) : cmul(p, x[r]);
+    }
+  }
+}
+
+// One quad tile: NT stage-1 members (A = NT-2, B = NT-1), NS summed bits,
+// K0: member 0 is the real |+> scale.
+template <int NT, int NS, int K0>
+__device__ __forceinline__ void chain_tile4(ChainWarp4& cw, const SegOpTab* __restrict__ tab,
+                                            const DevSeg& sg, V* __restrict__ arena,
+                                            uint32_t tile, int lane) {
+  constexpr int IA = NT - 2, IB = NT - 1;
+  constexpr int P0 = K0 ? 1 : 0;  // first gathered prefix member
+  const int L = sg.nst;
+  const uint32_t nj = 1u << (L - 1);
+  const V* Bp[NT];
+  uint32_t o[NT], sdl[NT], d0[NT];
+  const R r0 = K0 ? __ldg(&(arena + __ldg(&tab[0].off))->x) : R(0);
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    Bp[t] = arena + __ldg(&tab[t].off);
+    o[t] = cw.b.toff[t] + __ldg(&tab[t].llane[lane]);
+    sdl[t] = __ldg(&tab[t].sd);
+    d0[t] = __ldg(&tab[t].dj[0]);
+  }
+  const uint32_t da = cw.da[IA], db = cw.db[IB];
+  const DevStage st2 = cw.b.st[1];
+  V* y = arena + sg.out + (static_cast<uint64_t>(tile) << kSegYBits) + lane;
+  const uint64_t ya = uint64_t{1} << (sg.rb + kSegYBits), yb = uint64_t{1} << (sg.rb2 + kSegYBits);
+  for (uint32_t j = 0; j < nj; j += 2) {
+    if (j) {
+      const int b = __ffs(j) - 1;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t];
+    }
+    V x[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      V h[4];
+#pragma unroll
+      for (int s = 0; s <= NS; ++s) {
+        const uint32_t oa = o[IA] + (q ? d0[IA] : 0u) + (s ? sdl[IA] : 0u);
+        const uint32_t ob = o[IB] + (q ? d0[IB] : 0u) + (s ? sdl[IB] : 0u);
+        const V a0 = ld(Bp[IA] + oa), a1 = ld(Bp[IA] + oa + da);
+        const V b0 = ld(Bp[IB] + ob), b1 = ld(Bp[IB] + ob + db);
+        V pa0, pa1;
+        if constexpr (IA == P0) {  // no gathered prefix
+          pa0 = K0 ? rscale(r0, a0) : a0;
+          pa1 = K0 ? rscale(r0, a1) : a1;
+        } else {
+          V pf = ld(Bp[P0] + o[P0] + (q ? d0[P0] : 0u) + (s ? sdl[P0] : 0u));
+          if (K0) pf = rscale(r0, pf);
+#pragma unroll
+          for (int t = P0 + 1; t < IA; ++t)
+            pf = cmul(pf, ld(Bp[t] + o[t] + (q ? d0[t] : 0u) + (s ? sdl[t] : 0u)));
+          pa0 = cmul(pf, a0);
+          pa1 = cmul(pf, a1);
+        }
+        const V t0 = cmul(pa0, b0), t1 = cmul(pa1, b0), t2 = cmul(pa0, b1), t3 = cmul(pa1, b1);
+        if (s == 0) {
+          h[0] = t0;
+          h[1] = t1;
+          h[2] = t2;
+          h[3] = t3;
+        } else {
+          h[0] = cadd(h[0], t0);
+          h[1] = cadd(h[1], t1);
+          h[2] = cadd(h[2], t2);
+          h[3] = cadd(h[3], t3);
+        }
+      }
+      chain_term4(cw, tab, arena, st2, 0, j | static_cast<uint32_t>(q), h, lane);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) x[r] = q ? cadd(x[r], h[r]) : h[r];
+    }
+    const uint32_t jj = j | 1u;
+    bool carry = true;
+    for (int k = 1; k + 2 <= L; ++k) {
+      chain_term4(cw, tab, arena, cw.b.st[k + 1], k, jj, x, lane);
+      if (!((jj >> k) & 1u)) {
+        cw.b.acc[k - 1][lane] = x[0];
+        cw.b.acc1[k - 1][lane] = x[1];
+        cw.acc2[k - 1][lane] = x[2];
+        cw.acc3[k - 1][lane] = x[3];
+        carry = false;
+        break;
+      }
+      x[0] = cadd(cw.b.acc[k - 1][lane], x[0]);
+      x[1] = cadd(cw.b.acc1[k - 1][lane], x[1]);
+      x[2] = cadd(cw.acc2[k - 1][lane], x[2]);
+      x[3] = cadd(cw.acc3[k - 1][lane], x[3]);
+    }
+    if (carry) {
+      y[0] = x[0];
+      y[ya] = x[1];
+      y[yb] = x[2];
+      y[ya + yb] = x[3];
+    }
+  }
+}
+
+// One work item of the loaded quad segment (the tile number without bits rb, rb2).
+__device__ __forceinline__ void seg_tile4(ChainWarp4& cw, SegCursor& sc, uint32_t item,
+                                          const DevTensor* __restrict__ trefs,
+                                          const SegOpTab* __restrict__ segtab,
+                                          V* __restrict__ arena, int lane) {
+  const DevSeg& sg = sc.sg;
+  const SegOpTab* tab = segtab + sg.tref;
+  const uint32_t lo = min(sg.rb, sg.rb2), hi = max(sg.rb, sg.rb2);
+  const uint32_t tile = insert_zero(insert_zero(item, lo), hi);
+  for (int op = 0; op < sg.nops; ++op) {
+    const uint32_t v = ((tile >> lane) & 1u) ? __ldg(&tab[op].dtile[lane]) : 0u;
+    const uint32_t sum = __reduce_add_sync(kFull, v);
+    if (lane == 0) cw.b.toff[op] = sum;
+  }
+  if (!sc.ptab_fresh || sc.ptab_tile) {
+    chain_ptab_build(cw.b, sg, trefs, arena, tile, lane, static_cast<uint8_t>(kTileSrc + sg.rb),
+                     static_cast<uint8_t>(kTileSrc + sg.rb2));
+    sc.ptab_fresh = true;
+  }
+  __syncwarp();
+  const DevStage s1 = cw.b.st[0];
+  const bool k0 = s1.nt >= 3 && __ldg(&tab[0].kind) == kTensorRealScalar;
+  switch (s1.nt * 4 + s1.ns * 2 + (k0 ? 1 : 0)) {
+    case 8: chain_tile4<2, 0, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 10: chain_tile4<2, 1, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 12: chain_tile4<3, 0, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 13: chain_tile4<3, 0, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 14: chain_tile4<3, 1, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 15: chain_tile4<3, 1, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 16: chain_tile4<4, 0, 0>(cw, tab, sg, arena, tile, lane); break;
+    case 17: chain_tile4<4, 0, 1>(cw, tab, sg, arena, tile, lane); break;
+    case 18: chain_tile4<4, 1, 0>(cw, tab, sg, arena, tile, lane); break;
+    default: chain_tile4<4, 1, 1>(cw, tab, sg, arena, tile, lane); break;
+  }
+  __syncwarp();
+}
+
+#ifndef QTNG_SEG4_MINB
+#define QTNG_SEG4_MINB 20  // resident seg4_kernel warps per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(32, QTNG_SEG4_MINB)
+seg4_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
+            const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
+            const SegOpTab* __restrict__ segtab, V* __restrict__ arena, uint32_t seg_count,
+            uint32_t items, uint32_t* ctr) {
+  __shared__ ChainWarp4 cw;
+  const int lane = threadIdx.x & 31;
+  SegCursor sc;
+  uint32_t cur_begin = 0, cur_end = 0;
+  uint32_t nxt = 0;
+  if (lane == 0) nxt = atomicAdd(ctr, 1u);
+  for (;;) {
+    const uint32_t item = __shfl_sync(kFull, nxt, 0);
+    if (item >= items) break;
+    if (lane == 0) nxt = atomicAdd(ctr, 1u);
+    if (sc.cur < 0 || item < cur_begin || item >= cur_end) {
+      uint32_t lo = 0, hi = seg_count;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ibeg + mid) <= item) lo = mid; else hi = mid;
+      }
+      if (static_cast<int>(lo) != sc.cur) {
+        seg_switch(cw.b, sc, segs, static_cast<int>(lo), stages, segtab, lane, true);
+        seg_switch4(cw, sc.sg, segtab + sc.sg.tref, lane);
+      }
+      cur_begin = __ldg(ibeg + lo);
+      cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
+    }
+    seg_tile4(cw, sc, item - cur_begin, trefs, segtab, arena, lane);
+  }
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every warp has left the queue
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
 }
 
 #ifndef QTNG_SEG_MINB
@@ -1351,6 +1658,30 @@ cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_
   seg_kernel<<<seg_grid(lv.seg_items), 32 * kSegWarps, 0, s>>>(
       segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, trefs, segtab, arena, lv.seg_count,
       lv.seg_items, ctr);
+  return cudaGetLastError();
+}
+
+int seg4_grid(uint32_t items) {
+  static int cap = 0;
+  if (cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg4_kernel, 32, 0);
+    cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return static_cast<int>(items < static_cast<uint32_t>(cap) ? (items > 0 ? items : 1) : cap);
+}
+
+cudaError_t launch_segs4(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
+                         const DevStage* stages, const DevTensor* trefs, const SegOpTab* segtab,
+                         void* arena_v, uint32_t* ctr, const LevelLaunch& lv) {
+  if (lv.seg4_items == 0) return cudaSuccess;
+  V* arena = static_cast<V*>(arena_v);
+  const uint32_t first = lv.seg_begin + lv.seg_count;
+  seg4_kernel<<<seg4_grid(lv.seg4_items), 32, 0, s>>>(segs + first, seg_ibeg + first, stages, trefs,
+                                                      segtab, arena, lv.seg4_count, lv.seg4_items,
+                                                      ctr);
   return cudaGetLastError();
 }
 

@@ -30,6 +30,12 @@ namespace qtng {
                           const DevStage* stages, const DevTensor* trefs,                     \
                           const SegOpTab* segtab, void* arena, uint32_t* ctr,                  \
                           const LevelLaunch& lv);                                              \
+  /* the level's quad-tile segments (seg4_kernel), concurrent with the others; */            \
+  /* ctr: its own queue counters */                                                            \
+  cudaError_t launch_segs4(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,       \
+                           const DevStage* stages, const DevTensor* trefs,                    \
+                           const SegOpTab* segtab, void* arena, uint32_t* ctr,                 \
+                           const LevelLaunch& lv);                                             \
   /* the segments' SegOpTab entries (once per descriptor upload) */                           \
   cudaError_t launch_seg_prep(cudaStream_t s, const DevSeg* segs, uint32_t n_segs,             \
                               const DevTensor* trefs, SegOpTab* segtab);                       \
@@ -55,9 +61,10 @@ QTNG_KERNEL_API
 }  // namespace c64
 
 // Number of kernels launched per plan execution (level kernels, outer-join
-// kernels, segment kernels, final).
-inline int kernels_per_plan(int n_level_launches, int n_outer_launches, int n_seg_launches) {
-  return n_level_launches + n_outer_launches + n_seg_launches + 1;
+// kernels, segment kernels, quad segment kernels, final).
+inline int kernels_per_plan(int n_level_launches, int n_outer_launches, int n_seg_launches,
+                            int n_seg4_launches = 0) {
+  return n_level_launches + n_outer_launches + n_seg_launches + n_seg4_launches + 1;
 }
 
 }  // namespace qtng

@@ -126,6 +126,16 @@ int seg_pair_max_nt() {
   return t;
 }
 
+// Segments of levels with at least this many tiles use quad tiles when their
+// head is an outer join (DevSeg::rb2; QTNG_SEG_QUAD, default 8192; 0 disables).
+uint64_t seg_quad_min_tiles() {
+  static const uint64_t t = [] {
+    const char* v = std::getenv("QTNG_SEG_QUAD");
+    return static_cast<uint64_t>(v ? std::atoll(v) : 8192);
+  }();
+  return t;
+}
+
 uint64_t seg_starved_tiles() {
   static const uint64_t t = [] {
     const char* v = std::getenv("QTNG_SEG_STARVED");
@@ -404,7 +414,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   {
     uint32_t io = 0, is = 0, ist = 0;
     for (int L = 0; L < n_levels; ++L) {
-      LevelLaunch ll{io, 0, 0, 0, 0, 0, is, 0, 0};
+      LevelLaunch ll{io, 0, 0, 0, 0, 0, is, 0, 0, 0, 0};
       for (uint32_t i = lstart[L]; i < lstart[L + 1]; ++i) {
         const uint32_t u = order[i];
         unit_tref[u] = n_trefs;
@@ -424,6 +434,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
           sg.cy = static_cast<uint8_t>(seg_cy(u));
           sg.nops = static_cast<uint8_t>(unit_nops[u]);
           sg.rb = kNoVar;  // chosen with the operand maps below
+          sg.rb2 = kNoVar;
           sg.item_begin = ll.seg_items;
           hp.seg_ibeg[is - 1] = ll.seg_items;
           const uint64_t tiles = uint64_t{1} << (o.r - sg.cy);
@@ -564,10 +575,63 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
         // the summed vars of this stage never reappear
         if (seg) for (int k = 0; k < o.ns; ++k) pm_stamp[sv[k]] = 0;
       }
+      bool quad = false;
+      if (seg && !flow && cy == kSegYBits && ry >= cy + 2 && seg_quad_min_tiles() &&
+          level_tiles[unit_level[u]] >= seg_quad_min_tiles()) {
+        // quad tiles: stage 1 = [prefix..., A, B] with a tile bit A reads
+        // alone (rb) and one B reads alone (rb2); prefer the pair whose rows
+        // the fewest side products depend on (a stage-i side member reading
+        // a row bit is formed per row, 2^(L-i) times per tile row)
+        DevSeg& sg = hp.segs[unit_slot[u]];
+        const DevStage* sts = hp.stages.data() + unit_stage[u];
+        const int nt = sts[0].nt;
+        auto tile_bits = [&](const DevTensor& x) {
+          uint32_t b = 0;
+          for (int ax = 0; ax < x.rank; ++ax)
+            if (x.src[ax] >= kTileSrc && x.src[ax] < kSumSrc) b |= 1u << (x.src[ax] - kTileSrc);
+          return b;
+        };
+        if (nt >= 2 && nt <= kSegQuadMaxNt && sts[0].ns <= 1) {
+          const DevTensor* m1 = hp.trefs.data() + unit_tref[u] + sts[0].op0;
+          const DevTensor& A = m1[nt - 2];
+          const DevTensor& B = m1[nt - 1];
+          uint32_t pre = 0;
+          for (int t = 0; t < nt - 2; ++t) pre |= tile_bits(m1[t]);
+          const uint32_t ta = tile_bits(A), tb = tile_bits(B);
+          const uint32_t aonly = ta & ~tb & ~pre, bonly = tb & ~ta & ~pre;
+          if (aonly && bonly && A.kind != kTensorRealScalar && B.kind != kTensorRealScalar) {
+            uint64_t cost[32] = {};  // per tile bit: side products made per row
+            for (int i = 1; i < sg.nst; ++i)
+              for (int t = 0; t < sts[i].nt; ++t) {
+                if (t == sts[i].main) continue;
+                const uint32_t b = tile_bits(hp.trefs[unit_tref[u] + sts[i].op0 + t]);
+                for (int k = 0; k < 32; ++k)
+                  if ((b >> k) & 1u) cost[k] |= uint64_t{1} << (sg.nst - 1 - i);
+              }
+            int ba = -1, bb = -1;
+            uint64_t best = ~uint64_t{0};
+            for (int a = 0; a < ry - cy; ++a) {
+              if (!((aonly >> a) & 1u)) continue;
+              for (int b = 0; b < ry - cy; ++b) {
+                if (!((bonly >> b) & 1u)) continue;
+                const uint64_t c = cost[a] | cost[b];
+                if (c < best) {
+                  best = c;
+                  ba = a;
+                  bb = b;
+                }
+              }
+            }
+            sg.rb = static_cast<uint8_t>(ba);
+            sg.rb2 = static_cast<uint8_t>(bb);
+            quad = true;
+          }
+        }
+      }
       if (!seg) {
         DevOp& d = hp.ops[unit_slot[u]];
         mark_invariant_lead(d, hp.trefs.data() + d.tref);
-      } else if (cy == kSegYBits && ry > cy && seg_pair_min_tiles() &&
+      } else if (!quad && cy == kSegYBits && ry > cy && seg_pair_min_tiles() &&
                  hp.stages[unit_stage[u]].nt <= seg_pair_max_nt() &&
                  level_tiles[unit_level[u]] >= seg_pair_min_tiles()) {
         // paired rows: a tile bit no side member reads, preferring one that
@@ -603,32 +667,42 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     std::vector<DevSeg> tmp;
     auto tile_cost = [&](const DevSeg& sg) {
       return (uint64_t{1} << (sg.nst - 1)) * (sg.nops + hp.stages[sg.stage].nt) *
-             (sg.rb != kNoVar ? 2u : 1u);
+             (sg.rb2 != kNoVar ? 4u : sg.rb != kNoVar ? 2u : 1u);
     };
-    for (const LevelLaunch& ll : hp.levels) {
+    // quad segments go last (their own kernel and tile queue), each group in
+    // decreasing tile cost
+    for (LevelLaunch& ll : hp.levels) {
       perm.resize(ll.seg_count);
       for (uint32_t k = 0; k < ll.seg_count; ++k) perm[k] = ll.seg_begin + k;
       std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+        const bool qa = hp.segs[a].rb2 != kNoVar, qb = hp.segs[b].rb2 != kNoVar;
+        if (qa != qb) return qb;
         return tile_cost(hp.segs[a]) > tile_cost(hp.segs[b]);
       });
+      uint32_t nq = 0;
+      for (uint32_t k = 0; k < ll.seg_count; ++k) nq += hp.segs[perm[k]].rb2 != kNoVar;
+      ll.seg4_count = nq;
       tmp.resize(ll.seg_count);
       for (uint32_t k = 0; k < ll.seg_count; ++k) {
         tmp[k] = hp.segs[perm[k]];
         slot_of[perm[k]] = ll.seg_begin + k;
       }
       std::copy(tmp.begin(), tmp.end(), hp.segs.begin() + ll.seg_begin);
+      ll.seg_count -= nq;
     }
     for (uint32_t u = 0; u < U; ++u)
       if (unit_len[u] > 1) unit_slot[u] = slot_of[unit_slot[u]];
   }
   for (LevelLaunch& ll : hp.levels) {
     ll.seg_items = 0;
-    for (uint32_t k = ll.seg_begin; k < ll.seg_begin + ll.seg_count; ++k) {
+    ll.seg4_items = 0;
+    for (uint32_t k = ll.seg_begin; k < ll.seg_begin + ll.seg_count + ll.seg4_count; ++k) {
       DevSeg& sg = hp.segs[k];
-      const uint64_t tiles = uint64_t{1} << (sg.ry - sg.cy - (sg.rb != kNoVar ? 1 : 0));
-      sg.item_begin = ll.seg_items;
-      hp.seg_ibeg[k] = ll.seg_items;
-      ll.seg_items += static_cast<uint32_t>(tiles);
+      const uint64_t tiles = uint64_t{1} << seg_item_bits(sg);
+      uint32_t& acc = k < ll.seg_begin + ll.seg_count ? ll.seg_items : ll.seg4_items;
+      sg.item_begin = acc;
+      hp.seg_ibeg[k] = acc;
+      acc += static_cast<uint32_t>(tiles);
     }
   }
   for (int e : chunk_err) {
@@ -675,7 +749,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       f.idx = unit_slot[u];
       if (f.kind) {
         const DevSeg& sg = hp.segs[f.idx];
-        f.n_items = 1u << (sg.ry - sg.cy - (sg.rb != kNoVar ? 1 : 0));
+        f.n_items = 1u << seg_item_bits(sg);
       } else {
         const DevOp& d = hp.ops[f.idx];
         f.n_items = 1u << (d.r - d.cb);

@@ -70,25 +70,40 @@ def test_segment_shapes(q, golden):
             assert mem[main][0] == 0  # placeholder: read from registers
             assert all(rank > 0 for rank, _, _ in mem[:main])
         # stage i's result rank shrinks by its summed var: rY = r_1 - (L - 1)
-        if s["rb"] is not None:
+        if s["rb2"] is not None:
+            # quad tiles: stage 1 = [prefix..., A, B]; rb read by A alone, rb2 by B alone
+            assert s["cy"] == 5 and 2 <= nt1 <= 4 and s["rb"] != s["rb2"]
+            mem1 = s["stages"][0][3]
+            ca, cb = 32 + s["rb"], 32 + s["rb2"]
+            assert ca in mem1[-2][2] and cb not in mem1[-2][2]
+            assert cb in mem1[-1][2] and ca not in mem1[-1][2]
+            assert all(ca not in c and cb not in c for _, _, c in mem1[:-2])
+        elif s["rb"] is not None:
             # paired rows: full lane tiles, a tile bit that no side member reads
             assert s["cy"] == 5 and 0 <= s["rb"] < s["ry"] - 5 and nt1 <= 4
             for nt, ns, main, mem in s["stages"][1:]:
                 for t, (rank, _, codes) in enumerate(mem):
                     assert t == main or 32 + s["rb"] not in codes
-    assert any(s["rb"] is not None for s in segs)
+    assert any(s["rb2"] is not None for s in segs)
 
 
 def test_pairing_switch(q, golden):
-    # QTNG_SEG_PAIR=0 disables paired rows (read once per process: child)
+    # QTNG_SEG_PAIR=0 disables paired rows, QTNG_SEG_QUAD=0 quad tiles (read
+    # once per process: child)
     c, p = _cfg(golden, "C2")
     code = ("import sys; sys.path.insert(0, %r); import paper_2204_06045_b200 as q; "
             "g = q.random_regular(%d, 3, %d); "
-            "print(sum(s['rb'] is not None for s in q.plan_segments(g, %d)))") % (ROOT, c["n"], c["seed"], p)
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, QTNG_SEG_PAIR="0"),
-                       capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr[-2000:]
-    assert int(r.stdout.strip().splitlines()[-1]) == 0
+            "print(sum(s['rb'] is not None and s['rb2'] is None for s in q.plan_segments(g, %d)), "
+            "sum(s['rb2'] is not None for s in q.plan_segments(g, %d)))") % (
+                ROOT, c["n"], c["seed"], p, p)
+    for env, want in (({"QTNG_SEG_PAIR": "0"}, lambda pr, qd: pr == 0 and qd > 0),
+                      ({"QTNG_SEG_QUAD": "0"}, lambda pr, qd: pr > 0 and qd == 0),
+                      ({"QTNG_SEG_QUAD": "0", "QTNG_SEG_PAIR": "0"}, lambda pr, qd: pr == qd == 0)):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        pr, qd = (int(x) for x in r.stdout.strip().splitlines()[-1].split())
+        assert want(pr, qd), (env, pr, qd)
 
 
 def _child_energy(name, env):
@@ -117,7 +132,10 @@ def test_fused_equals_unfused_bitwise(golden, name):
     plain = _child_energy(name, {"QTNG_FUSE": "0"})
     assert plain["segments"] == 0
     for env in ({"QTNG_SEG_J": "1"}, {"QTNG_SEG_J": "3"}, {"QTNG_SEG_J": "8"},
-                {"QTNG_SEG_PAIR": "0"}, {"QTNG_SEG_PAIR": "1"}, {"QTNG_SEG_PAIR_NT": "2"}):
+                {"QTNG_SEG_PAIR": "0"}, {"QTNG_SEG_PAIR": "1"}, {"QTNG_SEG_PAIR_NT": "2"},
+                {"QTNG_SEG_QUAD": "0"}, {"QTNG_SEG_QUAD": "1"},
+                {"QTNG_SEG_QUAD": "1", "QTNG_SEG_J": "2"},
+                {"QTNG_SEG_QUAD": "0", "QTNG_SEG_PAIR": "0"}):
         fused = _child_energy(name, env)
         assert fused["segments"] > 0
         assert fused["terms"] == plain["terms"], str(env)

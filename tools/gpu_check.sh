@@ -20,7 +20,7 @@ sys.path.insert(0, '.')
 import paper_2204_06045_b200 as q
 g, a = q.random_regular(30, 3, 104478), q.Angles([0.30, 0.25, 0.20, 0.15], [0.35, 0.30, 0.25, 0.20])
 plan = q.Plan(g, 4)
-for _ in range(3): plan.execute(a)
+for _ in range(3): plan.profile(a)
 print('levels', plan.info().n_levels, 'kernel_ms', plan.kernel_ms())
 print(' '.join('%.1f' % (1000 * x) for x in plan.level_ms()))
 PY

@@ -8,7 +8,7 @@ import numpy as np
 import paper_2204_06045_b200 as q
 g, a = q.random_regular(30, 3, 104478), q.Angles([0.30, 0.25, 0.20, 0.15], [0.35, 0.30, 0.25, 0.20])
 plan = q.Plan(g, 4)
-for _ in range(3): plan.execute(a)
+for _ in range(3): plan.profile(a)
 print('device ms', plan.last_device_ms)
 print(' '.join('%.1f' % (1000 * x) for x in plan.level_ms()))
 PY

@@ -8,7 +8,7 @@ import sys; sys.path.insert(0, %r)
 import paper_2204_06045_b200 as q
 g, a = q.random_regular(30, 3, 104478), q.Angles([0.30, 0.25, 0.20, 0.15], [0.35, 0.30, 0.25, 0.20])
 plan = q.Plan(g, 4)
-for _ in range(5): plan.execute(a)
+for _ in range(5): plan.profile(a)
 lv, k = plan.level_ms(), plan.level_kernel_ms()
 print("step", round(plan.run_device(20) / 20, 4))
 print("level_ms ", " ".join("%%.1f" %% (1e3 * x) for x in lv))

@@ -12,7 +12,7 @@ g, a = q.random_regular(30, 3, 104478), q.Angles([0.30, 0.25, 0.20, 0.15], [0.35
 shard = dist.lpt_shard(q.edge_costs(g, 4), n)[0]
 plan = q.Plan(g, 4, edges=shard)
 for _ in range(3):
-    plan.execute(a)
+    plan.profile(a)
 lv, k = plan.level_ms(), plan.level_kernel_ms()
 print("edges", len(shard), "levels", len(lv), "graph ms", plan.run_device(10) / 10)
 for L in range(len(lv)):

@@ -10,13 +10,13 @@ import paper_2204_06045_b200 as q
 g = q.random_regular(30, 3, 104478); a = q.Angles([0.30,0.25,0.20,0.15],[0.35,0.30,0.25,0.20])
 ctx = q.Context(0); plan = q.Plan(g, 4, ctx=ctx)
 try:
-    t = plan.execute(a); e = 0.5*g.m - 0.5*float(np.sum(t.real))
+    t = plan.profile(a); e = 0.5*g.m - 0.5*float(np.sum(t.real))
 except Exception as ex:  # timing experiments may compute garbage
     e = repr(ex)[:60]
 for _ in range(3): plan.run_device(1)
 ms = plan.run_device(20) / 20
 try:
-    plan.execute(a)
+    plan.profile(a)
 except Exception:
     pass
 lv = plan.level_ms()
