@@ -345,7 +345,11 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
     if (kev) QTNG_CUDA(cudaEventRecord(kev[k], st));
   };
   if (fork2 || fork3 || fork4) QTNG_CUDA(cudaEventRecord(la.fork, la.s));
-  if (fork4) {  // quad-tile segments first: they are the level's longest kernel
+  static const bool seg4_first = [] {  // QTNG_SEG4_FIRST=0: quad kernel after seg_kernel
+    const char* v = std::getenv("QTNG_SEG4_FIRST");
+    return !(v && v[0] == '0');
+  }();
+  auto launch4 = [&] {
     QTNG_CUDA(cudaStreamWaitEvent(la.s4, la.fork, 0));
     rec(6, la.s4);
     QTNG_CUDA(c64 ? c64::launch_segs4(la.s4, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
@@ -354,7 +358,8 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
                                        pr.segtab(), arena, pr.ctr(level) + 2, lv));
     rec(7, la.s4);
     QTNG_CUDA(cudaEventRecord(la.join4, la.s4));
-  }
+  };
+  if (fork4 && seg4_first) launch4();
   if (fork2) {
     QTNG_CUDA(cudaStreamWaitEvent(la.s2, la.fork, 0));
     rec(2, la.s2);
@@ -372,6 +377,7 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
                                     pr.segtab(), arena, pr.ctr(level), lv));
   rec(5, s3);
   if (fork3) QTNG_CUDA(cudaEventRecord(la.join3, la.s3));
+  if (fork4 && !seg4_first) launch4();
   rec(0, la.s);
   QTNG_CUDA(c64 ? c64::launch_level(la.s, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv)
                 : c128::launch_level(la.s, pr.ops(), pr.ibeg(), pr.trefs(), arena, lv));

@@ -1000,11 +1000,11 @@ struct SegCursor {
 // table-index bits.
 __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const DevSeg* __restrict__ segs,
                                            int si, const DevStage* __restrict__ stages,
-                                           const SegOpTab* __restrict__ segtab, int lane,
-                                           bool quad = false) {
+                                           const SegOpTab* __restrict__ segtab, int lane) {
   sc.cur = si;
   sc.sg = segs[si];
   const DevSeg& sg = sc.sg;
+  const bool quad = sg.rb2 != kNoVar;
   __syncwarp();
   bool tile_dep = false;
   if (lane < sg.nst) {
@@ -1096,15 +1096,15 @@ __device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t 
 // l1tex__data_pipe_lsu_wavefronts 59% vs FP64 30%).
 // Each row sees exactly the unfused operation sequence: left fold in member
 // order ((prefix * A) * B), summed values ascending, the climb as in
-// chain_tile2; a side member that reads rb / rb2 is gathered (or looked up)
-// per row.
+// chain_tile2; a tabulated side product that depends on rb / rb2 is looked
+// up per row (build_plan never picks row bits a gathered side member reads).
 struct ChainWarp4 {
   ChainWarp b;                          // rows 0 / 1 park in b.acc / b.acc1
   V acc2[kSegMaxStages - 2][32];        // ... rows 2 / 3
   V acc3[kSegMaxStages - 2][32];
   uint32_t da[kSegMaxOps], db[kSegMaxOps];  // per operand: offset of tile bit rb / rb2
-  // per stage: bits 0-7 = ptab index bit fed by rb, 8-15 = by rb2; bit 16 / 17:
-  // a gathered side member reads rb / rb2
+  // per stage: bits 0-7 = ptab index bit fed by rb, 8-15 = by rb2 (a tabulated
+  // side product may depend on the row; gathered side members never do)
   uint32_t rdesc[kSegMaxStages];
 };
 
@@ -1126,46 +1126,10 @@ __device__ __forceinline__ void seg_switch4(ChainWarp4& cw, const DevSeg& sg,
         if (st.u[w] == ca) d |= 2u << w;
         if (st.u[w] == cb) d |= (2u << w) << 8;
       }
-    } else if (mode == 3u) {
-      for (int t = 0; t + 1 < st.nt; ++t) {
-        if (cw.da[st.op0 + t]) d |= 1u << 16;
-        if (cw.db[st.op0 + t]) d |= 1u << 17;
-      }
     }
     cw.rdesc[lane] = d;
   }
   __syncwarp();
-}
-
-// chain_side for row r of a quad tile (side members reading rb / rb2; cold:
-// kept out of line).
-__device__ __forceinline__ V chain_side_row(const ChainWarp4& cw, const SegOpTab* __restrict__ tab,
-                                            const V* __restrict__ arena, int op0, int m,
-                                            uint32_t j, int lane, int r, bool* real) {
-  const uint32_t jl = j & 15u, jh = j >> 4;
-  V p = mkv(0.0, 0.0);
-  bool pr = false;
-#pragma unroll
-  for (int t = 0; t < kSegMaxNt - 1; ++t) {
-    if (t >= m) break;
-    const int op = op0 + t;
-    const SegOpTab* tb = tab + op;
-    const bool xr = __ldg(&tb->kind) == kTensorRealScalar;
-    const V x = xr ? mkv(__ldg(&(arena + __ldg(&tb->off))->x), 0.0)
-                   : ld(arena + __ldg(&tb->off) +
-                        (cw.b.toff[op] + __ldg(&tb->llane[lane]) + __ldg(&tb->dlo[jl]) +
-                         __ldg(&tb->dhi[jh]) + ((r & 1) ? cw.da[op] : 0u) +
-                         ((r & 2) ? cw.db[op] : 0u)));
-    if (t == 0) {
-      p = x;
-      pr = xr;
-    } else {
-      p = fmul(p, pr, x, xr);
-      pr = false;
-    }
-  }
-  *real = pr;
-  return p;
 }
 
 // Stage k + 2's term for the four rows: x[r] = P(j, row r) * x[r].
@@ -1194,19 +1158,11 @@ __device__ __forceinline__ void chain_term4(const ChainWarp4& cw, const SegOpTab
     }
     return;
   }
-  if (!(rd >> 16)) {
-    bool real;
-    const V p = chain_side(cw.b, tab, arena, st.op0, st.nt - 1, j, lane, &real);
+  // gathered side members never read rb / rb2 (build_plan): one product for all rows
+  bool real;
+  const V p = chain_side(cw.b, tab, arena, st.op0, st.nt - 1, j, lane, &real);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) x[r] = real ? rscale(p.x, x[r]) : cmul(p, x[r]);
-  } else {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      bool real;
-      const V p = chain_side_row(cw, tab, arena, st.op0, st.nt - 1, j, lane, r, &real);
-      x[r] = real ? rscale(p.x, x[r]) : cmul(p, x[r]);
-    }
-  }
+  for (int r = 0; r < 4; ++r) x[r] = real ? rscale(p.x, x[r]) : cmul(p, x[r]);
 }
 
 // One quad tile: NT stage-1 members (A = NT-2, B = NT-1), NS summed bits,
@@ -1327,6 +1283,10 @@ __device__ __forceinline__ void seg_tile4(ChainWarp4& cw, SegCursor& sc, uint32_
   __syncwarp();
   const DevStage s1 = cw.b.st[0];
   const bool k0 = s1.nt >= 3 && __ldg(&tab[0].kind) == kTensorRealScalar;
+#ifdef QTNG_SASS_ONE_SHAPE
+  chain_tile4<3, 1, 1>(cw, tab, sg, arena, tile, lane);
+  return;
+#endif
   switch (s1.nt * 4 + s1.ns * 2 + (k0 ? 1 : 0)) {
     case 8: chain_tile4<2, 0, 0>(cw, tab, sg, arena, tile, lane); break;
     case 10: chain_tile4<2, 1, 0>(cw, tab, sg, arena, tile, lane); break;
@@ -1342,8 +1302,98 @@ __device__ __forceinline__ void seg_tile4(ChainWarp4& cw, SegCursor& sc, uint32_
   __syncwarp();
 }
 
+#ifndef QTNG_SEG_MINB
+#define QTNG_SEG_MINB 28  // resident seg_kernel warps per SM the register budget must allow (72 regs)
+#endif
+#ifndef QTNG_SEG_WARPS
+#define QTNG_SEG_WARPS 1  // warps per CTA (independent; fewer CTAs = less reserved shared memory)
+#endif
+#ifndef QTNG_SEG_GROUP
+#define QTNG_SEG_GROUP (QTNG_SEG_WARPS > 1)  // CTAs take consecutive items (L1 sharing)
+#endif
+constexpr int kSegWarps = QTNG_SEG_WARPS;
+__global__ void __launch_bounds__(32 * kSegWarps, QTNG_SEG_MINB / kSegWarps)
+seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
+           const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
+           const SegOpTab* __restrict__ segtab, V* __restrict__ arena, uint32_t seg_count,
+           uint32_t items, uint32_t* ctr) {
+#ifdef QTNG_NOOP_SEG  // launch-floor experiments only (tools/tune.py)
+  return;
+#endif
+  __shared__ ChainWarp cws[kSegWarps];
+  ChainWarp& cw = cws[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  // dynamic tile queue (segments are sorted by per-tile cost, largest first);
+  // ctr[0] = next tile, ctr[1] = finished warps (CTAs); the last one resets both
+  SegCursor sc;
+  uint32_t cur_begin = 0, cur_end = 0;
+#if QTNG_SEG_GROUP
+  // the CTA's warps take kSegWarps CONSECUTIVE items per round: neighbouring
+  // tiles share operand rows, so co-resident warps hit each other's L1 lines
+  __shared__ uint32_t blk[2];
+  const uint32_t wid = threadIdx.x >> 5;
+  int ph = 0;
+  if (threadIdx.x == 0) blk[0] = atomicAdd(ctr, static_cast<uint32_t>(kSegWarps));
+  __syncthreads();
+  for (;;) {
+    const uint32_t base = blk[ph];
+    if (base >= items) break;
+    if (threadIdx.x == 0) blk[ph ^ 1] = atomicAdd(ctr, static_cast<uint32_t>(kSegWarps));
+    const uint32_t item = base + wid;
+    if (item < items) {
+      if (sc.cur < 0 || item < cur_begin || item >= cur_end) {
+        uint32_t lo = 0, hi = seg_count;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (__ldg(ibeg + mid) <= item) lo = mid; else hi = mid;
+        }
+        if (static_cast<int>(lo) != sc.cur) seg_switch(cw, sc, segs, static_cast<int>(lo), stages, segtab, lane);
+        cur_begin = __ldg(ibeg + lo);
+        cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
+      }
+      seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane);
+    }
+    __syncthreads();
+    ph ^= 1;
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+  return;
+#endif
+  uint32_t nxt = 0;  // the next tile is fetched while the current one runs
+  if (lane == 0) nxt = atomicAdd(ctr, 1u);
+  for (;;) {
+    const uint32_t item = __shfl_sync(kFull, nxt, 0);
+    if (item >= items) break;
+    if (lane == 0) nxt = atomicAdd(ctr, 1u);
+    if (sc.cur < 0 || item < cur_begin || item >= cur_end) {
+      uint32_t lo = 0, hi = seg_count;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ibeg + mid) <= item) lo = mid; else hi = mid;
+      }
+      if (static_cast<int>(lo) != sc.cur) seg_switch(cw, sc, segs, static_cast<int>(lo), stages, segtab, lane);
+      cur_begin = __ldg(ibeg + lo);
+      cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
+    }
+    seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane);
+  }
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x * kSegWarps - 1) {  // every warp has left the queue
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
 #ifndef QTNG_SEG4_MINB
-#define QTNG_SEG4_MINB 20  // resident seg4_kernel warps per SM the register budget must allow
+#define QTNG_SEG4_MINB 16  // resident seg4_kernel warps per SM the register budget must allow (128 regs)
 #endif
 __global__ void __launch_bounds__(32, QTNG_SEG4_MINB)
 seg4_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
@@ -1367,7 +1417,7 @@ seg4_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
         if (__ldg(ibeg + mid) <= item) lo = mid; else hi = mid;
       }
       if (static_cast<int>(lo) != sc.cur) {
-        seg_switch(cw.b, sc, segs, static_cast<int>(lo), stages, segtab, lane, true);
+        seg_switch(cw.b, sc, segs, static_cast<int>(lo), stages, segtab, lane);
         seg_switch4(cw, sc.sg, segtab + sc.sg.tref, lane);
       }
       cur_begin = __ldg(ibeg + lo);
@@ -1378,55 +1428,6 @@ seg4_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
   if (lane == 0) {
     __threadfence();
     if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // every warp has left the queue
-      ctr[0] = 0;
-      ctr[1] = 0;
-    }
-  }
-}
-
-#ifndef QTNG_SEG_MINB
-#define QTNG_SEG_MINB 28  // resident seg_kernel warps per SM the register budget must allow (72 regs)
-#endif
-#ifndef QTNG_SEG_WARPS
-#define QTNG_SEG_WARPS 1  // warps per CTA (independent; fewer CTAs = less reserved shared memory)
-#endif
-constexpr int kSegWarps = QTNG_SEG_WARPS;
-__global__ void __launch_bounds__(32 * kSegWarps, QTNG_SEG_MINB / kSegWarps)
-seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
-           const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
-           const SegOpTab* __restrict__ segtab, V* __restrict__ arena, uint32_t seg_count,
-           uint32_t items, uint32_t* ctr) {
-#ifdef QTNG_NOOP_SEG  // launch-floor experiments only (tools/tune.py)
-  return;
-#endif
-  __shared__ ChainWarp cws[kSegWarps];
-  ChainWarp& cw = cws[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
-  // dynamic tile queue (segments are sorted by per-tile cost, largest first);
-  // ctr[0] = next tile, ctr[1] = finished warps; the last warp resets both
-  SegCursor sc;
-  uint32_t cur_begin = 0, cur_end = 0;
-  uint32_t nxt = 0;  // the next tile is fetched while the current one runs
-  if (lane == 0) nxt = atomicAdd(ctr, 1u);
-  for (;;) {
-    const uint32_t item = __shfl_sync(kFull, nxt, 0);
-    if (item >= items) break;
-    if (lane == 0) nxt = atomicAdd(ctr, 1u);
-    if (sc.cur < 0 || item < cur_begin || item >= cur_end) {
-      uint32_t lo = 0, hi = seg_count;
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(ibeg + mid) <= item) lo = mid; else hi = mid;
-      }
-      if (static_cast<int>(lo) != sc.cur) seg_switch(cw, sc, segs, static_cast<int>(lo), stages, segtab, lane);
-      cur_begin = __ldg(ibeg + lo);
-      cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
-    }
-    seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane);
-  }
-  if (lane == 0) {
-    __threadfence();
-    if (atomicAdd(ctr + 1, 1u) == gridDim.x * kSegWarps - 1) {  // every warp has left the queue
       ctr[0] = 0;
       ctr[1] = 0;
     }

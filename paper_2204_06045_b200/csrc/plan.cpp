@@ -126,14 +126,70 @@ int seg_pair_max_nt() {
   return t;
 }
 
-// Segments of levels with at least this many tiles use quad tiles when their
-// head is an outer join (DevSeg::rb2; QTNG_SEG_QUAD, default 8192; 0 disables).
+// Segments of levels with at least this many tiles may use quad tiles when
+// their head is an outer join (DevSeg::rb2; QTNG_SEG_QUAD, default 65536 --
+// a quad tile is a quarter of the work items, so smaller levels starve; 0
+// disables).  Measured on C2 (graph replay): 8192 / 16384 / 32768 / 65536 ->
+// 2.32 / 2.30 / 2.29 / 2.27 ms vs 2.32 ms without quad tiles.
 uint64_t seg_quad_min_tiles() {
   static const uint64_t t = [] {
     const char* v = std::getenv("QTNG_SEG_QUAD");
-    return static_cast<uint64_t>(v ? std::atoll(v) : 8192);
+    return static_cast<uint64_t>(v ? std::atoll(v) : 65536);
   }();
   return t;
+}
+
+// Quad-tile segments run in their own kernel (seg4_kernel: its own register
+// budget and tile queue, concurrent with seg_kernel).
+bool seg4_split() { return true; }
+
+// Quad tiles are used when their row score is below this multiple of the
+// paired / single-row score (QTNG_SEG_QUAD_MARGIN, default 1.2: the score
+// counts loads only, and a quad row also saves FP64 work and side lookups).
+double seg_quad_margin() {
+  static const double m = [] {
+    const char* v = std::getenv("QTNG_SEG_QUAD_MARGIN");
+    return v ? std::atof(v) : 1.2;
+  }();
+  return m;
+}
+
+// Tile-number bits (Y bits above the lanes) an operand of a segment reads.
+uint32_t seg_tile_bits(const DevTensor& x) {
+  uint32_t b = 0;
+  for (int ax = 0; ax < x.rank; ++ax)
+    if (x.src[ax] >= kTileSrc && x.src[ax] < kSumSrc) b |= 1u << (x.src[ax] - kTileSrc);
+  return b;
+}
+
+// Operand loads per output row and tile pass of a segment whose lanes each
+// compute the rows spanned by the tile bits `rows` (see the row-tiling
+// choice in build_plan).  tr: the segment's DevTensors.
+double seg_row_score(const DevSeg& sg, const DevStage* sts, const DevTensor* tr, uint32_t rows) {
+  const int J = sg.nst - 1;
+  double loads = 0.0;
+  for (int t = 0; t < sts[0].nt; ++t) {
+    const DevTensor& x = tr[sts[0].op0 + t];
+    if (x.kind == kTensorRealScalar) continue;
+    loads += std::ldexp(1.0, J + sts[0].ns + __builtin_popcount(seg_tile_bits(x) & rows));
+  }
+  for (int i = 1; i < sg.nst; ++i) {
+    const double terms = std::ldexp(1.0, J - i + 1);
+    if (sts[i].ptab) {
+      int nr = 0;
+      for (int w = 0; w < 2; ++w)
+        if (sts[i].u[w] >= kTileSrc && sts[i].u[w] < kSumSrc && ((rows >> (sts[i].u[w] - kTileSrc)) & 1u)) ++nr;
+      loads += 0.5 * terms * std::ldexp(1.0, nr);
+      continue;
+    }
+    for (int t = 0; t < sts[i].nt; ++t) {
+      if (t == sts[i].main) continue;
+      const DevTensor& x = tr[sts[i].op0 + t];
+      if (x.kind == kTensorRealScalar) continue;
+      loads += terms * std::ldexp(1.0, __builtin_popcount(seg_tile_bits(x) & rows));
+    }
+  }
+  return loads / std::ldexp(1.0, __builtin_popcount(rows));
 }
 
 uint64_t seg_starved_tiles() {
@@ -575,56 +631,60 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
         // the summed vars of this stage never reappear
         if (seg) for (int k = 0; k < o.ns; ++k) pm_stamp[sv[k]] = 0;
       }
+      // Row tiling of the segment's lanes (DevSeg::rb / rb2).  Score = operand
+      // loads per output row and tile pass (the L1 data path that a load's
+      // register write-back occupies is seg_kernel's bound): stage-1 members
+      // load per digit assignment and summed value once per distinct row they
+      // read; a stage-i side member once per term (2^(J-i+1) terms) and
+      // distinct row, a tabulated side product at half a load.
       bool quad = false;
+      double quad_score = 0.0;
       if (seg && !flow && cy == kSegYBits && ry >= cy + 2 && seg_quad_min_tiles() &&
           level_tiles[unit_level[u]] >= seg_quad_min_tiles()) {
         // quad tiles: stage 1 = [prefix..., A, B] with a tile bit A reads
-        // alone (rb) and one B reads alone (rb2); prefer the pair whose rows
-        // the fewest side products depend on (a stage-i side member reading
-        // a row bit is formed per row, 2^(L-i) times per tile row)
+        // alone (rb) and one B reads alone (rb2)
         DevSeg& sg = hp.segs[unit_slot[u]];
         const DevStage* sts = hp.stages.data() + unit_stage[u];
         const int nt = sts[0].nt;
-        auto tile_bits = [&](const DevTensor& x) {
-          uint32_t b = 0;
-          for (int ax = 0; ax < x.rank; ++ax)
-            if (x.src[ax] >= kTileSrc && x.src[ax] < kSumSrc) b |= 1u << (x.src[ax] - kTileSrc);
-          return b;
-        };
         if (nt >= 2 && nt <= kSegQuadMaxNt && sts[0].ns <= 1) {
           const DevTensor* m1 = hp.trefs.data() + unit_tref[u] + sts[0].op0;
           const DevTensor& A = m1[nt - 2];
           const DevTensor& B = m1[nt - 1];
           uint32_t pre = 0;
-          for (int t = 0; t < nt - 2; ++t) pre |= tile_bits(m1[t]);
-          const uint32_t ta = tile_bits(A), tb = tile_bits(B);
+          for (int t = 0; t < nt - 2; ++t) pre |= seg_tile_bits(m1[t]);
+          const uint32_t ta = seg_tile_bits(A), tb = seg_tile_bits(B);
           const uint32_t aonly = ta & ~tb & ~pre, bonly = tb & ~ta & ~pre;
           if (aonly && bonly && A.kind != kTensorRealScalar && B.kind != kTensorRealScalar) {
-            uint64_t cost[32] = {};  // per tile bit: side products made per row
-            for (int i = 1; i < sg.nst; ++i)
-              for (int t = 0; t < sts[i].nt; ++t) {
-                if (t == sts[i].main) continue;
-                const uint32_t b = tile_bits(hp.trefs[unit_tref[u] + sts[i].op0 + t]);
-                for (int k = 0; k < 32; ++k)
-                  if ((b >> k) & 1u) cost[k] |= uint64_t{1} << (sg.nst - 1 - i);
-              }
+            // row bits no gathered side member reads (its product is shared
+            // by the four rows; tabulated ones are looked up per row)
+            uint32_t gside = 0;
+            const DevTensor* tr = hp.trefs.data() + unit_tref[u];
+            for (int i = 1; i < sg.nst; ++i) {
+              if (sts[i].ptab) continue;
+              for (int t = 0; t < sts[i].nt; ++t)
+                if (t != sts[i].main) gside |= seg_tile_bits(tr[sts[i].op0 + t]);
+            }
             int ba = -1, bb = -1;
-            uint64_t best = ~uint64_t{0};
+            double best = 0.0;
             for (int a = 0; a < ry - cy; ++a) {
-              if (!((aonly >> a) & 1u)) continue;
+              if (!((aonly >> a) & 1u) || ((gside >> a) & 1u)) continue;
               for (int b = 0; b < ry - cy; ++b) {
-                if (!((bonly >> b) & 1u)) continue;
-                const uint64_t c = cost[a] | cost[b];
-                if (c < best) {
-                  best = c;
+                if (!((bonly >> b) & 1u) || ((gside >> b) & 1u)) continue;
+                const double sc = seg_row_score(sg, sts, hp.trefs.data() + unit_tref[u],
+                                                (1u << a) | (1u << b));
+                if (ba < 0 || sc < best) {
+                  best = sc;
                   ba = a;
                   bb = b;
                 }
               }
             }
-            sg.rb = static_cast<uint8_t>(ba);
-            sg.rb2 = static_cast<uint8_t>(bb);
-            quad = true;
+            if (ba >= 0) {
+              sg.rb = static_cast<uint8_t>(ba);
+              sg.rb2 = static_cast<uint8_t>(bb);
+              quad = true;
+              quad_score = best;
+            }
           }
         }
       }
@@ -655,6 +715,45 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
           if (!((side >> b) & 1u) && (best < 0 || n1[b] < n1[best])) best = b;
         if (best >= 0) sg.rb = static_cast<uint8_t>(best);
       }
+      if (quad) {  // quad tiles only where they beat paired rows (or one row) clearly
+        DevSeg& sg = hp.segs[unit_slot[u]];
+        const DevStage* sts = hp.stages.data() + unit_stage[u];
+        const DevTensor* tr = hp.trefs.data() + unit_tref[u];
+        double alt = seg_row_score(sg, sts, tr, 0u);
+        if (cy == kSegYBits && ry > cy && seg_pair_min_tiles() &&
+            hp.stages[unit_stage[u]].nt <= seg_pair_max_nt() &&
+            level_tiles[unit_level[u]] >= seg_pair_min_tiles()) {
+          uint32_t side = 0;
+          for (int i = 1; i < sg.nst; ++i)
+            for (int t = 0; t < sts[i].nt; ++t)
+              if (t != sts[i].main) side |= seg_tile_bits(tr[sts[i].op0 + t]);
+          for (int b = 0; b < ry - cy; ++b)
+            if (!((side >> b) & 1u)) alt = std::min(alt, seg_row_score(sg, sts, tr, 1u << b));
+        }
+        if (!(quad_score < seg_quad_margin() * alt)) {
+          // undo: fall back to the paired / single choice
+          sg.rb = kNoVar;
+          sg.rb2 = kNoVar;
+          quad = false;
+          uint32_t side = 0, n1[32] = {};
+          for (int i = 0; i < sg.nst; ++i)
+            for (int t = 0; t < sts[i].nt; ++t) {
+              if (i > 0 && t == sts[i].main) continue;
+              const uint32_t b = seg_tile_bits(tr[sts[i].op0 + t]);
+              for (int k = 0; k < 32; ++k)
+                if ((b >> k) & 1u) {
+                  if (i > 0) side |= 1u << k; else ++n1[k];
+                }
+            }
+          if (cy == kSegYBits && ry > cy && seg_pair_min_tiles() &&
+              sts[0].nt <= seg_pair_max_nt() && level_tiles[unit_level[u]] >= seg_pair_min_tiles()) {
+            int best = -1;
+            for (int b = 0; b < ry - cy; ++b)
+              if (!((side >> b) & 1u) && (best < 0 || n1[b] < n1[best])) best = b;
+            if (best >= 0) sg.rb = static_cast<uint8_t>(best);
+          }
+        }
+      }
       unit_dev_bytes[u] = dev_bytes;
     }
   });
@@ -667,7 +766,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     std::vector<DevSeg> tmp;
     auto tile_cost = [&](const DevSeg& sg) {
       return (uint64_t{1} << (sg.nst - 1)) * (sg.nops + hp.stages[sg.stage].nt) *
-             (sg.rb2 != kNoVar ? 4u : sg.rb != kNoVar ? 2u : 1u);
+             (sg.rb2 != kNoVar ? 3u : sg.rb != kNoVar ? 2u : 1u);  // a quad tile costs ~3
     };
     // quad segments go last (their own kernel and tile queue), each group in
     // decreasing tile cost
@@ -675,12 +774,13 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       perm.resize(ll.seg_count);
       for (uint32_t k = 0; k < ll.seg_count; ++k) perm[k] = ll.seg_begin + k;
       std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
-        const bool qa = hp.segs[a].rb2 != kNoVar, qb = hp.segs[b].rb2 != kNoVar;
+        const bool qa = seg4_split() && hp.segs[a].rb2 != kNoVar;
+        const bool qb = seg4_split() && hp.segs[b].rb2 != kNoVar;
         if (qa != qb) return qb;
         return tile_cost(hp.segs[a]) > tile_cost(hp.segs[b]);
       });
-      uint32_t nq = 0;
-      for (uint32_t k = 0; k < ll.seg_count; ++k) nq += hp.segs[perm[k]].rb2 != kNoVar;
+      uint32_t nq = 0;  // QTNG_SEG4_SPLIT=1: quad segments in their own kernel
+      for (uint32_t k = 0; k < ll.seg_count && seg4_split(); ++k) nq += hp.segs[perm[k]].rb2 != kNoVar;
       ll.seg4_count = nq;
       tmp.resize(ll.seg_count);
       for (uint32_t k = 0; k < ll.seg_count; ++k) {

@@ -13,6 +13,6 @@ for v in "$@"; do
        -I../../include $flags -DQTNG_C64=1 -c kernels.cu -o ../../build/variants/k64_$tag.o
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../build/variants/libqtng_$tag.so \
        ../../build/obj/host.o ../../build/obj/walk.o ../../build/obj/plan.o ../../build/obj/capi.o \
-       ../../build/obj/sv.o ../../build/variants/k_$tag.o ../../build/variants/k64_$tag.o -lpthread
+       ../../build/obj/sv.o ../../build/obj/peak.o ../../build/variants/k_$tag.o ../../build/variants/k64_$tag.o -lpthread
   echo "$tag: $(grep -A2 seg_kernel ../../build/variants/ptxas_$tag.txt | grep -E 'registers|spill' | tr '\n' ' ' | tr -s ' ')"
 done

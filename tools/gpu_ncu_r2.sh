@@ -10,12 +10,12 @@ rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
 h = rows[0]; ii, ki, mi, vi = (h.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value"))
 t = {}
 for r in rows[1:]:
-    if r[mi] == "gpu__time_duration.sum" and "seg_kernel" in r[ki]:
+    if r[mi] == "gpu__time_duration.sum" and (__import__("os").environ.get("KRE","seg_kernel")) in r[ki]:
         t[int(r[ii])] = float(r[vi].replace(",", ""))
 ids = sorted(t); half = len(ids) // 2
 print(max(range(half, len(ids)), key=lambda k: t[ids[k]]))
 PY
 )
 echo "segskip=$SEGSKIP" >> $O/ncu.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s ${SEGSKIP:-30} -c 1 -o $O/seg python tools/profile_step.py step >> $O/ncu.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KRE:-seg_kernel} -s ${SEGSKIP:-30} -c 1 -o $O/seg python tools/profile_step.py step >> $O/ncu.txt 2>&1
 echo "ncu rc=$?" >> $O/ncu.txt
