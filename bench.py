@@ -22,8 +22,9 @@ Multi-GPU: edges LPT-sharded by predicted work (the library's qtng_shard_edges,
 the placement its single-process driver qtng_energy_multi uses too), one NCCL
 reduce of the terms (total work fixed as N grows: "strong" scaling).
 Sub-records (N=1, rank 0): `c4` (N=100 p=3, the 8-GPU config, on one GPU:
-value, e2e, parity), `c64` (C2 in the complex64 mode: value, error), and
-`multi_api` (qtng_energy_multi on this one device: the C-ABI multi-GPU path).
+value, e2e, parity), `c64` (C2 in the complex64 mode: value, error),
+`multi_api` (qtng_energy_multi on this one device: the C-ABI multi-GPU path)
+and `merged` (C2 with merge_buckets: value, e2e, parity).
 --impl reference: the reference's own energy_expectation (oracle/_ref, built
 from /root/reference unmodified), matmul backend, jobs = all host threads.
 """
@@ -351,6 +352,8 @@ def run_b200(args, cfg):
         if args.dtype == "c128":
             subs["c64"] = sub_c64(q, ctx, cfg, args)
         subs["multi_api"] = sub_multi(q, ctx, cfg, args)
+        if args.dtype == "c128":
+            subs["merged"] = sub_merged(q, ctx, cfg, args)
     mpk_ma, mpk_fma = measured_fp64_peak(q, local)
 
     if rank != 0:
@@ -527,6 +530,41 @@ def sub_c64(q, ctx, cfg, args, steps=10):
     return {"value": g.m / (dev_ms / 1e3), "unit": "lightcones/s", "ms_per_step": dev_ms,
             "dtype": "c64", "energy": e, "rel_err_vs_c128_golden": abs(e - gold) / abs(gold),
             "tolerance": 1e-5}
+
+
+def sub_merged(q, ctx, cfg, args, steps=10):
+    """C2 with merge_buckets (engine.cpp:306-358): merged buckets sum up to 9
+    vars at once and run in the level kernel's multi-sum path; device value,
+    one-shot e2e and parity against the reference's naive merged energy."""
+    import numpy as np
+    g = q.random_regular(cfg["n"], cfg["d"], cfg["seed"])
+    a = q.Angles(cfg["gammas"], cfg["betas"])
+    plan = q.Plan(g, a.depth(), merged=True, ctx=ctx)
+    plan.execute(a)
+    plan.run_device(3)
+    dev_ms = plan.run_device(steps) / steps
+    t = plan.terms()
+    plan.profile(a)
+    kms = plan.kernel_ms()
+    info = plan.info()
+    plan.close()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        res = q.energy_expectation(g, a, q.GpuBackend(ctx), merged=True)
+    e2e_ms = 1e3 * (time.perf_counter() - t0) / 3
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "merged.json")) as f:
+            gold = json.load(f)["C2"]
+        ref = np.array([complex(x, y) for x, y in gold["terms_naive"]])
+        exact = bool(np.array_equal(t, ref)) and res.energy == gold["energy_naive"]
+        e_gold = gold["energy_naive"]
+    except Exception:
+        exact, e_gold = None, None
+    return {"value": g.m / (dev_ms / 1e3), "unit": "lightcones/s", "ms_per_step": dev_ms,
+            "e2e_ms_per_step": e2e_ms, "energy": res.energy, "energy_golden_naive_merged": e_gold,
+            "parity_bit_exact": exact, "merges_applied": res.report.merges_applied,
+            "eager_kernel_ms": kms, "levels": int(info.n_levels), "buckets": int(info.n_buckets),
+            "dev_bytes": info.dev_bytes, "fp64_ops": info.fp64_ops}
 
 
 def sub_multi(q, ctx, cfg, args, steps=5):

@@ -14,7 +14,9 @@ for _ in range(20):
     t0 = time.perf_counter(); r = q.energy_expectation(g, a, q.GpuBackend(ctx)); ts.append(time.perf_counter() - t0)
 ts.sort(); print("median ms %%.3f min %%.3f energy %%r" %% (1e3 * ts[10], 1e3 * ts[0], r.energy))
 ''' % ROOT
-for k in ("1", "2", "3", "4"):
-    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, QTNG_PIPELINE=k),
-                         capture_output=True, text=True, timeout=300)
-    print("lanes", k, out.stdout.strip(), out.stderr[-200:], flush=True)
+for order in ("0", "1"):
+    for k in ("1", "2", "3", "4"):
+        out = subprocess.run([sys.executable, "-c", code],
+                             env=dict(os.environ, QTNG_PIPELINE=k, QTNG_PIPELINE_ORDER=order),
+                             capture_output=True, text=True, timeout=300)
+        print("order", order, "lanes", k, out.stdout.strip(), out.stderr[-200:], flush=True)
