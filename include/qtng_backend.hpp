@@ -19,15 +19,20 @@
 //   * a sum var absent from the bucket throws qtnsim::ScheduleError with the
 //     reference's message (engine.cpp:28-36); other failures map onto the
 //     reference's exception types;
-//   * const and thread-safe: the context serialises device work, so the
-//     reference's `jobs` worker threads may share one backend.
+//   * const and thread-safe: every calling thread gets its own device context
+//     (stream, arena, staging) from a pool owned by the backend, so the
+//     reference's `jobs` worker threads contract their buckets concurrently
+//     (engine.cpp:531-541; "usable from multiple workers").
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <complex>
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "qtng.h"
@@ -38,11 +43,13 @@ namespace qtng {
 
 class GpuBackend final : public qtnsim::ContractionBackend {
  public:
-  explicit GpuBackend(int device = 0, uint64_t arena_bytes = 0) {
-    if (qtng_create(device, arena_bytes, &ctx_) != QTNG_OK)
-      throw std::runtime_error(std::string("qtng_create: ") + qtng_last_error());
+  explicit GpuBackend(int device = 0, uint64_t arena_bytes = 0)
+      : device_(device), arena_bytes_(arena_bytes), id_(next_id()) {
+    ctx_for_thread();  // fail at construction if the device is unusable
   }
-  ~GpuBackend() override { qtng_destroy(ctx_); }
+  ~GpuBackend() override {
+    for (qtng_ctx* c : pool_) qtng_destroy(c);
+  }
   GpuBackend(const GpuBackend&) = delete;
   GpuBackend& operator=(const GpuBackend&) = delete;
 
@@ -68,7 +75,7 @@ class GpuBackend final : public qtnsim::ContractionBackend {
     out.data.resize(static_cast<size_t>(cap));
     int rank = 0;
     const qtng_status st = qtng_contract_bucket(
-        ctx_, static_cast<int>(b.tensors.size()), ranks.data(), vars.data(), data.data(),
+        ctx_for_thread(), static_cast<int>(b.tensors.size()), ranks.data(), vars.data(), data.data(),
         static_cast<int>(b.sum_vars.size()), b.sum_vars.data(), &rank, out.vars.data(),
         reinterpret_cast<double*>(out.data.data()), cap);
     if (st != QTNG_OK) raise(st);
@@ -89,7 +96,32 @@ class GpuBackend final : public qtnsim::ContractionBackend {
       default: throw std::runtime_error(msg);
     }
   }
-  qtng_ctx* ctx_ = nullptr;
+  static uint64_t next_id() {
+    static std::atomic<uint64_t> n{0};
+    return ++n;
+  }
+  // The calling thread's context (created on its first bucket).  Keyed by a
+  // per-backend id, not the address, so a later backend at the same address
+  // never sees a stale entry.
+  qtng_ctx* ctx_for_thread() const {
+    thread_local std::unordered_map<uint64_t, qtng_ctx*> mine;
+    const auto it = mine.find(id_);
+    if (it != mine.end()) return it->second;
+    qtng_ctx* c = nullptr;
+    if (qtng_create(device_, arena_bytes_, &c) != QTNG_OK)
+      throw std::runtime_error(std::string("qtng_create: ") + qtng_last_error());
+    {
+      std::lock_guard<std::mutex> lk(pool_mu_);
+      pool_.push_back(c);
+    }
+    mine[id_] = c;
+    return c;
+  }
+  int device_;
+  uint64_t arena_bytes_;
+  uint64_t id_;
+  mutable std::mutex pool_mu_;
+  mutable std::vector<qtng_ctx*> pool_;
 };
 
 }  // namespace qtng

@@ -7,6 +7,7 @@
 // oracle/_ref/dropin_energy (needs the reference headers + objects and the
 // product library); run on the GPU box by tests/test_gpu_dropin.py.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -18,7 +19,41 @@
 
 using namespace qtnsim;
 
+// "time" mode: the reference's energy_expectation through the per-bucket
+// drop-in (GpuBackend::contract -> qtng_contract_bucket, one host round trip
+// per bucket), serial and with `jobs` worker threads, wall-clock each.
+int time_mode(int n, unsigned long long seed, int p, int jobs) {
+  Angles a;
+  const double g4[] = {0.30, 0.25, 0.20, 0.15}, b4[] = {0.35, 0.30, 0.25, 0.20};
+  for (int k = 0; k < p; ++k) {  // the acceptance-scale angles (acceptance.cpp:70-71)
+    a.gammas.push_back(g4[k % 4]);
+    a.betas.push_back(b4[k % 4]);
+  }
+  const Graph g = random_regular(n, 3, seed);
+  qtng::GpuBackend gpu(0);
+  energy_expectation(g, a, gpu, false);  // warm-up (context, arena)
+  auto wall = [&](int j, double* e, size_t* nrec) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const EnergyResult r = energy_expectation(g, a, gpu, false, {}, j);
+    *e = r.energy;
+    *nrec = r.report.records.size();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  double e1 = 0, ej = 0;
+  size_t r1 = 0, rj = 0;
+  const double t1 = wall(1, &e1, &r1), tj = wall(jobs, &ej, &rj);
+  std::printf("{\"mode\": \"time\", \"n\": %d, \"seed\": %llu, \"p\": %d, \"buckets\": %zu, "
+              "\"energy_jobs1\": %.17g, \"wall_s_jobs1\": %.6f, \"jobs\": %d, "
+              "\"energy_jobsN\": %.17g, \"wall_s_jobsN\": %.6f}\n",
+              n, seed, p, r1, e1, t1, jobs, ej, tj);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "time")
+    return time_mode(argc > 2 ? std::atoi(argv[2]) : 30,
+                     argc > 3 ? std::strtoull(argv[3], nullptr, 10) : 104478ull,
+                     argc > 4 ? std::atoi(argv[4]) : 4, argc > 5 ? std::atoi(argv[5]) : 16);
   const int n = argc > 1 ? std::atoi(argv[1]) : 10;
   const unsigned long long seed = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 7;
   const int p = argc > 3 ? std::atoi(argv[3]) : 1;

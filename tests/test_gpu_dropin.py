@@ -28,3 +28,18 @@ def test_reference_driver_with_b200_backend(n, seed, p):
     assert r["mixed_bad_dispatch"] == 0 and r["mixed_gpu_records"] > 0
     assert r["peak_b200"] == r["peak_naive"]
     assert r["refusal"].startswith("edge (") and "exceeds cap 3" in r["refusal"]
+
+
+@pytest.mark.skipif(not os.path.exists(BIN), reason="oracle/_ref/dropin_energy not built")
+def test_reference_driver_c2_timed(golden):
+    """C2 through the per-bucket drop-in (7,857 qtng_contract_bucket round
+    trips), serial and with 16 reference worker threads: the energy equals the
+    reference's naive energy; the wall times are printed for the record."""
+    c = golden["configs"]["C2"]
+    out = subprocess.run([BIN, "time", "30", str(c["seed"]), "4", "16"], capture_output=True,
+                         text=True, timeout=900, check=True).stdout
+    r = json.loads(out.strip().splitlines()[-1])
+    print("DROPIN", json.dumps(r))
+    assert r["buckets"] == c["n_records"]
+    assert r["energy_jobs1"] == c["energy_naive"]
+    assert r["energy_jobsN"] == c["energy_naive"]

@@ -41,3 +41,20 @@ PY
 )
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s ${SEGSKIP:-27} -c 1 -o $O/seg python tools/profile_step.py step >> $O/ncu.txt 2>&1
 echo "ncu rc=$?" >> $O/ncu.txt
+# the longest seg4_kernel (quad tiles) launch of the profiled step
+SEG4SKIP=$(python - "$O/launches.csv" <<'PY'
+import csv, sys
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
+h = rows[0]; ii, ki, mi, vi = (h.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value"))
+t = {}
+for r in rows[1:]:
+    if r[mi] == "gpu__time_duration.sum" and "seg4_kernel" in r[ki]:
+        t[int(r[ii])] = float(r[vi].replace(",", ""))
+ids = sorted(t); half = len(ids) // 2
+print(max(range(half, len(ids)), key=lambda k: t[ids[k]]) if ids else -1)
+PY
+)
+if [ "${SEG4SKIP:--1}" -ge 0 ]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg4_kernel -s $SEG4SKIP -c 1 -o $O/seg4 python tools/profile_step.py step >> $O/ncu.txt 2>&1
+  echo "ncu seg4 rc=$?" >> $O/ncu.txt
+fi

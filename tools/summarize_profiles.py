@@ -108,6 +108,10 @@ def main():
         out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"),
                               os.path.join(src, "seg.ncu-rep"), "30"], capture_output=True, text=True).stdout
         open(os.path.join(dst, "ncu_seg_kernel.txt"), "w").write(out)
+    if os.path.exists(os.path.join(src, "seg4.ncu-rep")):
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"),
+                              os.path.join(src, "seg4.ncu-rep"), "30"], capture_output=True, text=True).stdout
+        open(os.path.join(dst, "ncu_seg4_kernel.txt"), "w").write(out)
     print("wrote", dst)
 
 
