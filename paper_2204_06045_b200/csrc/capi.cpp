@@ -290,6 +290,7 @@ struct qtng_ctx {
   // default arithmetic of QAOA plans / energies whose call passes precision 0:
   // 128 = complex128, 64 = complex64.  Read once per call (atomic).
   std::atomic<int> prec{128};
+  std::atomic<int> refs{1};  // the owner + one per live plan (ctx_release)
 
   // arena of `elems` elements of `elem_bytes` (16: double2, 8: float2)
   void ensure_arena(uint64_t elems, size_t elem_bytes = sizeof(double2)) {
@@ -579,8 +580,15 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
   });
 }
 
-void qtng_destroy(qtng_ctx* ctx) {
-  if (!ctx) return;
+}  // extern "C"
+
+namespace {
+
+// Frees a context once neither its owner (qtng_destroy) nor any plan created
+// on it (qtng_plan_destroy) holds it: plans may outlive the qtng_destroy call
+// (garbage-collected bindings destroy in any order).
+void ctx_release(qtng_ctx* ctx) {
+  if (ctx->refs.fetch_sub(1) != 1) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->stream2);
@@ -609,6 +617,14 @@ void qtng_destroy(qtng_ctx* ctx) {
   delete ctx;  // frees the arenas and staging buffers
   for (cudaStream_t st : streams)
     if (st) cudaStreamDestroy(st);
+}
+
+}  // namespace
+
+extern "C" {
+
+void qtng_destroy(qtng_ctx* ctx) {
+  if (ctx) ctx_release(ctx);
 }
 
 qtng_status qtng_set_precision(qtng_ctx* ctx, int bits) {
@@ -915,6 +931,7 @@ qtng_status qtng_plan_create(qtng_ctx* ctx, int n, int m, const int* edges, int 
     plan->ker_ev.resize(8 * hp.levels.size());
     for (cudaEvent_t& e : plan->ker_ev) QTNG_CUDA(cudaEventCreate(&e));
     plan->level_ms.assign(hp.levels.size(), 0.f);
+    ctx->refs.fetch_add(1);  // released by qtng_plan_destroy
     *out = plan.release();
   });
 }
@@ -953,6 +970,7 @@ qtng_status qtng_plan_create_schedule(qtng_ctx* ctx, int n_buckets, const int* i
     plan->ker_ev.resize(8 * hp.levels.size());
     for (cudaEvent_t& e : plan->ker_ev) QTNG_CUDA(cudaEventCreate(&e));
     plan->level_ms.assign(hp.levels.size(), 0.f);
+    ctx->refs.fetch_add(1);  // released by qtng_plan_destroy
     *out = plan.release();
   });
 }
@@ -1291,9 +1309,13 @@ qtng_status qtng_plan_level_ms(const qtng_plan* plan, float* ms, int cap) {
 
 void qtng_plan_destroy(qtng_plan* plan) {
   if (!plan) return;
-  std::lock_guard<std::mutex> lk(plan->ctx->mu);
-  cudaSetDevice(plan->ctx->device);
-  delete plan;
+  qtng_ctx* ctx = plan->ctx;
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaSetDevice(ctx->device);
+    delete plan;
+  }
+  ctx_release(ctx);  // the plan's reference
 }
 
 qtng_status qtng_plan_time_level(qtng_plan* plan, int level, int n_runs, int* level_out,

@@ -138,3 +138,16 @@ def test_precision_is_per_call(q, ctx, golden):
     r64 = q.energy_expectation(g, a, q.GpuBackend(ctx), cfg=q.EngineConfig(dtype="c64"))
     assert abs(r64.energy - c["energy_naive"]) <= 1e-5 * c["energy_naive"]
     assert q.energy_expectation(g, a, q.GpuBackend(ctx)).energy == c["energy_naive"]
+
+
+def test_plan_outlives_its_context(q, golden):
+    """A plan keeps its context alive (garbage-collected bindings may destroy
+    the context first): it still executes, and freeing it frees the context."""
+    c = golden["configs"]["C1"]
+    g = q.random_regular(c["n"], 3, c["seed"])
+    own = q.Context(0)
+    plan = q.Plan(g, 1, ctx=own)
+    own.close()
+    t = plan.execute(q.Angles(c["gammas"], c["betas"]))
+    assert np.array_equal(t, _terms(c))
+    plan.close()
