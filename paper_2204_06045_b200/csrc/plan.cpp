@@ -98,8 +98,10 @@ class ClassArena {
 // segments give more, cheaper tiles; longer ones cut HBM traffic further).
 int seg_max_j() {
   static const int j = [] {
+    // 4 (measured, with quad tiles): C2 2.24 ms vs 2.28 ms at J = 5; 8-way
+    // shard floor 0.53 vs 0.59 ms
     const char* v = std::getenv("QTNG_SEG_J");
-    const int x = v ? std::atoi(v) : 5;
+    const int x = v ? std::atoi(v) : 4;
     return std::max(1, std::min(x, kSegMaxJ));
   }();
   return j;
@@ -127,14 +129,15 @@ int seg_pair_max_nt() {
 }
 
 // Segments of levels with at least this many tiles may use quad tiles when
-// their head is an outer join (DevSeg::rb2; QTNG_SEG_QUAD, default 65536 --
+// their head is an outer join (DevSeg::rb2; QTNG_SEG_QUAD, default 32768 --
 // a quad tile is a quarter of the work items, so smaller levels starve; 0
-// disables).  Measured on C2 (graph replay): 8192 / 16384 / 32768 / 65536 ->
-// 2.32 / 2.30 / 2.29 / 2.27 ms vs 2.32 ms without quad tiles.
+// disables).  Measured on C2 (graph replay, J = 5): 8192 / 16384 / 32768 /
+// 65536 -> 2.32 / 2.30 / 2.29 / 2.27 ms vs 2.32 ms without quad tiles; with
+// J = 4: 32768 -> 2.234, 65536 -> 2.243 ms.
 uint64_t seg_quad_min_tiles() {
   static const uint64_t t = [] {
     const char* v = std::getenv("QTNG_SEG_QUAD");
-    return static_cast<uint64_t>(v ? std::atoll(v) : 65536);
+    return static_cast<uint64_t>(v ? std::atoll(v) : 32768);
   }();
   return t;
 }
