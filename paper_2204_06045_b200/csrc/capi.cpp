@@ -204,7 +204,7 @@ ConeSet plan_cones(const Graph& g, int p, bool merged, int max_width, const std:
 struct DescLayout {
   size_t ops = 0, ibeg = 0, trefs = 0, segs = 0, seg_ibeg = 0, stages = 0, ctr = 0, scal = 0,
          lcb = 0, lce = 0, terms = 0, funits = 0, finit = 0, upload = 0, segtab = 0, fdone = 0, fdeps = 0,
-         fqueue = 0, fstate = 0, sscr = 0, sflg = 0, total = 0;
+         fqueue = 0, fstate = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t{255}; }
@@ -232,8 +232,6 @@ DescLayout layout_of(const HostPlan& hp) {
   L.fdeps = o; o = align256(o + nu * sizeof(int32_t));
   L.fqueue = o; o = align256(o + hp.flow_chunks * sizeof(uint64_t));
   L.fstate = o; o = align256(o + sizeof(FlowState));
-  L.sscr = o; o = align256(o + hp.split_items * 64 * sizeof(double2));  // split-tile scratch
-  L.sflg = o; o = align256(o + hp.split_items * sizeof(uint32_t));      // ... arrival counters
   L.total = o;
   return L;
 }
@@ -331,8 +329,6 @@ struct DevProgram {
   const uint32_t* lcb() const { return reinterpret_cast<const uint32_t*>(base + L.lcb); }
   const int32_t* lce() const { return reinterpret_cast<const int32_t*>(base + L.lce); }
   double2* terms() const { return reinterpret_cast<double2*>(base + L.terms); }
-  void* sscr() const { return base + L.sscr; }
-  uint32_t* sflg() const { return reinterpret_cast<uint32_t*>(base + L.sflg); }
 };
 
 // One level: the outer-join and segment kernels forked onto side streams, the
@@ -377,9 +373,9 @@ void enqueue_level(qtng_ctx* ctx, const LevelLaunch& lv, size_t level, const Dev
   if (fork3) QTNG_CUDA(cudaStreamWaitEvent(la.s3, la.fork, 0));
   rec(4, s3);
   QTNG_CUDA(c64 ? c64::launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
-                                    pr.segtab(), arena, pr.ctr(level), lv, pr.sscr(), pr.sflg())
+                                    pr.segtab(), arena, pr.ctr(level), lv)
                 : c128::launch_segs(s3, pr.segs(), pr.seg_ibeg(), pr.stages(), pr.trefs(),
-                                    pr.segtab(), arena, pr.ctr(level), lv, pr.sscr(), pr.sflg()));
+                                    pr.segtab(), arena, pr.ctr(level), lv));
   rec(5, s3);
   if (fork3) QTNG_CUDA(cudaEventRecord(la.join3, la.s3));
   if (fork4 && !seg4_first) launch4();
@@ -414,8 +410,6 @@ void upload_desc(qtng_ctx* ctx, const HostPlan& hp, const DescLayout& L, char* d
   pack_desc(hp, L, static_cast<char*>(la.pin_desc->p));
   QTNG_CUDA(cudaMemcpyAsync(dev, la.pin_desc->p, L.upload, cudaMemcpyHostToDevice, la.s));
   const DevProgram pr{dev, L, hp.c64};
-  if (hp.split_items)  // split-tile arrival counters start at zero (the kernels reset them)
-    QTNG_CUDA(cudaMemsetAsync(pr.sflg(), 0, hp.split_items * sizeof(uint32_t), la.s));
   if (!hp.segs.empty()) g_launches.fetch_add(1, std::memory_order_relaxed);
   QTNG_CUDA(c128::launch_seg_prep(la.s, pr.segs(), static_cast<uint32_t>(hp.segs.size()), pr.trefs(),
                             pr.segtab()));

@@ -117,22 +117,17 @@ struct alignas(16) DevSeg {
   // may read rb / rb2 (their products are then formed per row).  kNoVar:
   // not a quad segment.  A quad segment has a quarter as many work items.
   uint8_t rb2;
-  // Split tiles (latency-bound levels): each tile is two work items, h = item
-  // & 1 walking the digit assignments whose top digit is h; the last of the
-  // two to finish adds the other's top-stage term (in order: h = 0 first)
-  // from a scratch slot and stores Y.  Halves the sequential walk per warp.
-  uint8_t split;
-  uint8_t pad[5];
+  uint8_t pad[6];
 };
 static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
 
 // Per-operand tables of a segment, built on the device once per plan upload
 // (seg_prep_kernel) from the DevTensor bit maps and read by seg_kernel through
 // the read-only path.  Indexed like the DevTensor array.
-// log2 of a segment's work items: its tiles, halved for paired rows,
-// quartered for quad tiles, doubled for split tiles.
+// log2 of a segment's work items: its tiles, halved for paired rows and
+// quartered for quad tiles.
 inline int seg_item_bits(const DevSeg& sg) {
-  return sg.ry - sg.cy - (sg.rb2 != kNoVar ? 2 : (sg.rb != kNoVar ? 1 : 0)) + (sg.split ? 1 : 0);
+  return sg.ry - sg.cy - (sg.rb2 != kNoVar ? 2 : (sg.rb != kNoVar ? 1 : 0));
 }
 
 struct alignas(16) SegOpTab {

@@ -489,11 +489,6 @@ struct ChainWarp {
   V acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
   V acc1[kSegMaxStages - 2][32];   // ... of the second row (paired segments)
   uint32_t drow[kSegMaxNt1];       // paired: stage-1 member offset of the second row
-  // split tiles (DevSeg::split): this item's half, its level-wide index, and
-  // the plan's scratch slots / arrival counters
-  uint32_t split_on, split_h, split_item;
-  V* sscr;
-  uint32_t* sflg;
 };
 
 // (r, 0) * y and p * (r, 0): equal to cmul up to the sign of an exact zero.
@@ -593,32 +588,6 @@ __device__ __forceinline__ void chain_term2(const ChainWarp& cw, const SegOpTab*
   }
 }
 
-// End of one half of a split tile: the top stage's term(s) of this half go to
-// its scratch slot; the second half to arrive adds the two in order (half 0's
-// term first, as the sequential climb parks it) and stores Y.  Once per tile.
-__device__ __noinline__ void split_finish(const ChainWarp& cw, V t0, V t1, bool two, V* y0, V* y1,
-                                          int lane) {
-  V* mine = cw.sscr + static_cast<uint64_t>(cw.split_item) * 64;
-  mine[lane] = t0;
-  if (two) mine[32 + lane] = t1;
-  __threadfence();
-  __syncwarp();
-  const uint32_t fi = cw.split_item - cw.split_h;  // the tile's half-0 item
-  uint32_t old = 0;
-  if (lane == 0) old = atomicAdd(cw.sflg + fi, 1u);
-  old = __shfl_sync(kFull, old, 0);
-  if (old == 0) return;  // the other half finishes the tile
-  __threadfence();
-  const V* other = cw.sscr + static_cast<uint64_t>(cw.split_h ? cw.split_item - 1 : cw.split_item + 1) * 64;
-  const V o0 = __ldcg(other + lane);
-  *y0 = cw.split_h ? cadd(o0, t0) : cadd(t0, o0);
-  if (two) {
-    const V o1 = __ldcg(other + 32 + lane);
-    *y1 = cw.split_h ? cadd(o1, t1) : cadd(t1, o1);
-  }
-  if (lane == 0) cw.sflg[fi] = 0;  // ready for the next execution
-}
-
 // One paired tile (DevSeg::rb): chain_tile's walk with U = 1 for two Y rows
 // at once.  Row 1's stage-1 operands sit drow[t] further; everything else
 // (digit offsets, side products, climb control) is shared.  Each row sees
@@ -626,7 +595,7 @@ __device__ __noinline__ void split_finish(const ChainWarp& cw, V t0, V t1, bool 
 // stage-1 member t reads the row bit (drow[t] != 0); DM: bit t set if it
 // does not read digit bit 0 (dj[0] == 0).  Specialised for the common masks;
 // otherwise RM = all members, DM = none.
-template <int NT, int NS, int K0, int RM, int DM, bool SP = false>
+template <int NT, int NS, int K0, int RM, int DM>
 __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                             const DevSeg& sg, V* __restrict__ arena,
                                             uint32_t tile, int lane) {
@@ -646,18 +615,8 @@ __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __res
   const DevStage st2 = cw.st[1];
   V* y = arena + sg.out + (static_cast<uint64_t>(tile) << kSegYBits) + lane;
   const uint64_t y1 = uint64_t{1} << (sg.rb + kSegYBits);
-  // split tile (SP): this half walks the assignments whose top digit is split_h
-  constexpr bool split = SP;
-  uint32_t j0 = 0, jn = nj;
-  if (split) {
-    j0 = cw.split_h << (L - 2);
-    jn = j0 + (nj >> 1);
-    if (j0)
-#pragma unroll
-      for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].dj[L - 2]);
-  }
-  for (uint32_t j = j0; j < jn; j += 2) {
-    if (j != j0) {
+  for (uint32_t j = 0; j < nj; j += 2) {
+    if (j) {
       const int b = __ffs(j) - 1;
 #pragma unroll
       for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t];
@@ -717,11 +676,6 @@ __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __res
     bool carry = true;
     for (int k = 1; k + 2 <= L; ++k) {
       chain_term2(cw, tab, arena, cw.st[k + 1], k, jj, x0, x1, lane);
-      if (split && k + 2 == L) {
-        split_finish(cw, x0, x1, true, y, y + y1, lane);
-        carry = false;
-        break;
-      }
       if (!((jj >> k) & 1u)) {
         cw.acc[k - 1][lane] = x0;
         cw.acc1[k - 1][lane] = x1;
@@ -740,13 +694,13 @@ __device__ __forceinline__ void chain_tile2(ChainWarp& cw, const SegOpTab* __res
 
 // chain_tile2 specialised for the member masks key = RM | DM << 8 if it is
 // one of Keys.
-template <int NT, int NS, int K0, bool SP, int... Keys>
+template <int NT, int NS, int K0, int... Keys>
 __device__ __forceinline__ bool chain_tile2_masks(int key, ChainWarp& cw,
                                                   const SegOpTab* __restrict__ tab,
                                                   const DevSeg& sg, V* __restrict__ arena,
                                                   uint32_t tile, int lane) {
-  return ((key == Keys ? (chain_tile2<NT, NS, K0, (Keys & 0xff), (Keys >> 8), SP>(cw, tab, sg, arena,
-                                                                              tile, lane), true)
+  return ((key == Keys ? (chain_tile2<NT, NS, K0, (Keys & 0xff), (Keys >> 8)>(cw, tab, sg, arena,
+                                                                          tile, lane), true)
                        : false) || ...);
 }
 
@@ -754,7 +708,7 @@ __device__ __forceinline__ bool chain_tile2_masks(int key, ChainWarp& cw,
 // of 2^U consecutive j (stages 2..U+1 resolved in registers, four independent
 // stage-1 products in flight), then the climb above each group.
 // DM: bit t set if member t does not read digit bit 0 (loaded once per pair).
-template <int NT, int NS, int U, int K0, int DM = 0, bool SP = false>
+template <int NT, int NS, int U, int K0, int DM = 0>
 __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                            const DevSeg& sg, V* __restrict__ arena,
                                            uint32_t tile, int lane) {
@@ -776,18 +730,8 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
   }
   const DevStage st2 = cw.st[1];
   const DevStage st3 = U > 1 ? cw.st[2] : st2;
-  // split tile (SP, U == 1 only): this half walks the assignments whose top digit is split_h
-  constexpr bool split = SP && U == 1;
-  uint32_t j0 = 0, jn = nj;
-  if (split) {
-    j0 = cw.split_h << (L - 2);
-    jn = j0 + (nj >> 1);
-    if (j0)
-#pragma unroll
-      for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].dj[L - 2]);
-  }
-  for (uint32_t j = j0; j < jn; j += G) {
-    if (j != j0) {  // from j - G (low U bits clear) to j: inc[b] assumes bits < b were set
+  for (uint32_t j = 0; j < nj; j += G) {
+    if (j) {  // from j - G (low U bits clear) to j: inc[b] assumes bits < b were set
       const int b = __ffs(j) - 1;
 #pragma unroll
       for (int t = 0; t < NT; ++t) o[t] += __ldg(&tab[t].inc[b]) + d0[t] + d1[t];
@@ -837,12 +781,6 @@ __device__ __forceinline__ void chain_tile(ChainWarp& cw, const SegOpTab* __rest
     bool carry = true;
     for (int k = U; k + 2 <= L; ++k) {
       const V term = chain_term(cw, tab, arena, cw.st[k + 1], k, jj, x, lane);
-      if (split && k + 2 == L) {
-        V* yp = arena + sg.out + (static_cast<uint64_t>(tile) << sg.cy) + lane;
-        split_finish(cw, term, term, false, yp, yp, lane);
-        carry = false;
-        break;
-      }
       if (!((jj >> k) & 1u)) {
         cw.acc[k - 1][lane] = term;
         carry = false;
@@ -945,7 +883,7 @@ __device__ __noinline__ void chain_tile_lanes(ChainWarp& cw, const SegOpTab* __r
   }
 }
 
-template <int NT, int NS, bool SP = false>
+template <int NT, int NS>
 __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __restrict__ tab,
                                              const DevSeg& sg, V* __restrict__ arena,
                                              uint32_t tile, int lane) {
@@ -966,25 +904,25 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
         constexpr int K = NT >= 2 ? 1 : 0;
         key &= ~0x101;
         if constexpr (NS == 1 && NT == 3) {
-          if (chain_tile2_masks<3, 1, K, SP, 2, 4, 6 | 4 << 8>(key, cw, tab, sg, arena, tile, lane))
+          if (chain_tile2_masks<3, 1, K, 2, 4, 6 | 4 << 8>(key, cw, tab, sg, arena, tile, lane))
             return;
         }
         if constexpr (NS == 1 && NT == 4) {
-          if (chain_tile2_masks<4, 1, K, SP, 4, 8, 12, 12 | 2 << 8, 4 | 2 << 8, 8 | 2 << 8>(
+          if (chain_tile2_masks<4, 1, K, 4, 8, 12, 12 | 2 << 8, 4 | 2 << 8, 8 | 2 << 8>(
                   key, cw, tab, sg, arena, tile, lane))
             return;
         }
-        chain_tile2<NT, NS, K, kAll, 0, SP>(cw, tab, sg, arena, tile, lane);
+        chain_tile2<NT, NS, K, kAll, 0>(cw, tab, sg, arena, tile, lane);
       } else {
         if constexpr (NS == 1 && NT == 2) {
-          if (chain_tile2_masks<2, 1, 0, SP, 1, 2>(key, cw, tab, sg, arena, tile, lane)) return;
+          if (chain_tile2_masks<2, 1, 0, 1, 2>(key, cw, tab, sg, arena, tile, lane)) return;
         }
         if constexpr (NS == 1 && NT == 3) {
-          if (chain_tile2_masks<3, 1, 0, SP, 2, 4, 4 | 1 << 8, 2 | 1 << 8>(key, cw, tab, sg, arena,
+          if (chain_tile2_masks<3, 1, 0, 2, 4, 4 | 1 << 8, 2 | 1 << 8>(key, cw, tab, sg, arena,
                                                                       tile, lane))
             return;
         }
-        chain_tile2<NT, NS, 0, kAll, 0, SP>(cw, tab, sg, arena, tile, lane);
+        chain_tile2<NT, NS, 0, kAll, 0>(cw, tab, sg, arena, tile, lane);
       }
       return;
     }
@@ -998,12 +936,12 @@ __device__ __forceinline__ void chain_tile_u(ChainWarp& cw, const SegOpTab* __re
   if constexpr (NS == 1 && NT == 5) {  // the unpaired 5-member C2 head: members 1, 3 lack digit 0
     if (k0 && !__ldg(&tab[1].dj[0]) && __ldg(&tab[2].dj[0]) && !__ldg(&tab[3].dj[0]) &&
         __ldg(&tab[4].dj[0])) {
-      chain_tile<5, 1, 1, 1, 10, SP>(cw, tab, sg, arena, tile, lane);
+      chain_tile<5, 1, 1, 1, 10>(cw, tab, sg, arena, tile, lane);
       return;
     }
   }
-  if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0), 0, SP>(cw, tab, sg, arena, tile, lane);
-  else chain_tile<NT, NS, 1, 0, 0, SP>(cw, tab, sg, arena, tile, lane);
+  if (k0) chain_tile<NT, NS, 1, (NT >= 2 ? 1 : 0)>(cw, tab, sg, arena, tile, lane);
+  else chain_tile<NT, NS, 1, 0>(cw, tab, sg, arena, tile, lane);
 }
 
 // Tabulate the side products of the fused stages for this tile: lane
@@ -1105,17 +1043,10 @@ __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const D
 __device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t item,
                                          const DevTensor* __restrict__ trefs,
                                          const SegOpTab* __restrict__ segtab,
-                                         V* __restrict__ arena, int lane, uint32_t gitem = 0) {
+                                         V* __restrict__ arena, int lane) {
   const DevSeg& sg = sc.sg;
   const SegOpTab* tab = segtab + sg.tref;
-  // split: item = tile item << 1 | half; paired: the tile item is the tile
-  // number without bit rb (row 0 = bit clear)
-  if (lane == 0) {
-    cw.split_on = sg.split;
-    cw.split_h = item & 1u;
-    cw.split_item = gitem;
-  }
-  if (sg.split) item >>= 1;
+  // paired: the work item is the tile number without bit rb (row 0 = bit clear)
   const bool paired = sg.rb != kNoVar;
   const uint32_t tile = paired ? insert_zero(item, sg.rb) : item;
   if (paired && lane < kSegMaxNt1 && lane < sg.nops) cw.drow[lane] = __ldg(&tab[lane].dtile[sg.rb]);
@@ -1134,24 +1065,6 @@ __device__ __forceinline__ void seg_tile(ChainWarp& cw, SegCursor& sc, uint32_t 
   chain_tile_u<3, 1>(cw, tab, sg, arena, tile, lane);
   return;
 #endif
-  if (sg.split) {  // split tiles: latency-bound levels only
-    switch (s1.nt * 2 + s1.ns) {
-      case 2: chain_tile_u<1, 0, true>(cw, tab, sg, arena, tile, lane); break;
-      case 3: chain_tile_u<1, 1, true>(cw, tab, sg, arena, tile, lane); break;
-      case 4: chain_tile_u<2, 0, true>(cw, tab, sg, arena, tile, lane); break;
-      case 5: chain_tile_u<2, 1, true>(cw, tab, sg, arena, tile, lane); break;
-      case 6: chain_tile_u<3, 0, true>(cw, tab, sg, arena, tile, lane); break;
-      case 7: chain_tile_u<3, 1, true>(cw, tab, sg, arena, tile, lane); break;
-      case 8: chain_tile_u<4, 0, true>(cw, tab, sg, arena, tile, lane); break;
-      case 9: chain_tile_u<4, 1, true>(cw, tab, sg, arena, tile, lane); break;
-      case 10: chain_tile_u<5, 0, true>(cw, tab, sg, arena, tile, lane); break;
-      case 11: chain_tile_u<5, 1, true>(cw, tab, sg, arena, tile, lane); break;
-      case 12: chain_tile_u<6, 0, true>(cw, tab, sg, arena, tile, lane); break;
-      default: chain_tile_u<6, 1, true>(cw, tab, sg, arena, tile, lane); break;
-    }
-    __syncwarp();
-    return;
-  }
   switch (s1.nt * 2 + s1.ns) {
     case 2: chain_tile_u<1, 0>(cw, tab, sg, arena, tile, lane); break;
     case 3: chain_tile_u<1, 1>(cw, tab, sg, arena, tile, lane); break;
@@ -1403,17 +1316,13 @@ __global__ void __launch_bounds__(32 * kSegWarps, QTNG_SEG_MINB / kSegWarps)
 seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
            const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
            const SegOpTab* __restrict__ segtab, V* __restrict__ arena, uint32_t seg_count,
-           uint32_t items, uint32_t* ctr, V* sscr, uint32_t* sflg) {
+           uint32_t items, uint32_t* ctr) {
 #ifdef QTNG_NOOP_SEG  // launch-floor experiments only (tools/tune.py)
   return;
 #endif
   __shared__ ChainWarp cws[kSegWarps];
   ChainWarp& cw = cws[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    cw.sscr = sscr;
-    cw.sflg = sflg;
-  }
   // dynamic tile queue (segments are sorted by per-tile cost, largest first);
   // ctr[0] = next tile, ctr[1] = finished warps (CTAs); the last one resets both
   SegCursor sc;
@@ -1442,7 +1351,7 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
         cur_begin = __ldg(ibeg + lo);
         cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
       }
-      seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane, item);
+      seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane);
     }
     __syncthreads();
     ph ^= 1;
@@ -1472,7 +1381,7 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
       cur_begin = __ldg(ibeg + lo);
       cur_end = lo + 1 < seg_count ? __ldg(ibeg + lo + 1) : items;
     }
-    seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane, item);
+    seg_tile(cw, sc, item - cur_begin, trefs, segtab, arena, lane);
   }
   if (lane == 0) {
     __threadfence();
@@ -1744,13 +1653,12 @@ cudaError_t launch_seg_prep(cudaStream_t s, const DevSeg* segs, uint32_t n_segs,
 
 cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,
                         const DevStage* stages, const DevTensor* trefs, const SegOpTab* segtab,
-                        void* arena_v, uint32_t* ctr, const LevelLaunch& lv, void* split_scratch,
-                        uint32_t* split_flags) {
+                        void* arena_v, uint32_t* ctr, const LevelLaunch& lv) {
   if (lv.seg_items == 0) return cudaSuccess;
   V* arena = static_cast<V*>(arena_v);
   seg_kernel<<<seg_grid(lv.seg_items), 32 * kSegWarps, 0, s>>>(
       segs + lv.seg_begin, seg_ibeg + lv.seg_begin, stages, trefs, segtab, arena, lv.seg_count,
-      lv.seg_items, ctr, static_cast<V*>(split_scratch), split_flags);
+      lv.seg_items, ctr);
   return cudaGetLastError();
 }
 

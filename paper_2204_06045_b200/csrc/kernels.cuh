@@ -29,8 +29,7 @@ namespace qtng {
   cudaError_t launch_segs(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,        \
                           const DevStage* stages, const DevTensor* trefs,                     \
                           const SegOpTab* segtab, void* arena, uint32_t* ctr,                  \
-                          const LevelLaunch& lv, void* split_scratch,                          \
-                          uint32_t* split_flags);                                              \
+                          const LevelLaunch& lv);                                              \
   /* the level's quad-tile segments (seg4_kernel), concurrent with the others; */            \
   /* ctr: its own queue counters */                                                            \
   cudaError_t launch_segs4(cudaStream_t s, const DevSeg* segs, const uint32_t* seg_ibeg,       \

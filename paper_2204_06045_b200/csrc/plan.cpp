@@ -142,16 +142,6 @@ uint64_t seg_quad_min_tiles() {
   return t;
 }
 
-// Levels whose seg_kernel has fewer work items than this split their tiles
-// (DevSeg::split; QTNG_SEG_SPLIT, default 4096; 0 disables).
-uint64_t seg_split_items() {
-  static const uint64_t t = [] {
-    const char* v = std::getenv("QTNG_SEG_SPLIT");
-    return static_cast<uint64_t>(v ? std::atoll(v) : 4096);
-  }();
-  return t;
-}
-
 // Quad-tile segments run in their own kernel (seg4_kernel: its own register
 // budget and tile queue, concurrent with seg_kernel).
 bool seg4_split() { return true; }
@@ -504,7 +494,6 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
           sg.nops = static_cast<uint8_t>(unit_nops[u]);
           sg.rb = kNoVar;  // chosen with the operand maps below
           sg.rb2 = kNoVar;
-          sg.split = 0;
           sg.item_begin = ll.seg_items;
           hp.seg_ibeg[is - 1] = ll.seg_items;
           const uint64_t tiles = uint64_t{1} << (o.r - sg.cy);
@@ -807,22 +796,6 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     for (uint32_t u = 0; u < U; ++u)
       if (unit_len[u] > 1) unit_slot[u] = slot_of[unit_slot[u]];
   }
-  // split tiles on latency-bound levels: fewer seg_kernel items than
-  // QTNG_SEG_SPLIT (default 4096 ~ one per resident warp) -> every full-lane
-  // segment with >= 2 digits walks its tile in two halves
-  if (!flow && seg_split_items()) {
-    for (const LevelLaunch& ll : hp.levels) {
-      uint64_t items = 0;
-      for (uint32_t k = ll.seg_begin; k < ll.seg_begin + ll.seg_count; ++k)
-        items += uint64_t{1} << seg_item_bits(hp.segs[k]);
-      if (items == 0 || items >= seg_split_items()) continue;
-      for (uint32_t k = ll.seg_begin; k < ll.seg_begin + ll.seg_count; ++k) {
-        DevSeg& sg = hp.segs[k];
-        if (sg.cy == kSegYBits && sg.nst >= 3 && sg.rb2 == kNoVar) sg.split = 1;
-      }
-    }
-  }
-  hp.split_items = 0;
   for (LevelLaunch& ll : hp.levels) {
     ll.seg_items = 0;
     ll.seg4_items = 0;
@@ -834,9 +807,6 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
       hp.seg_ibeg[k] = acc;
       acc += static_cast<uint32_t>(tiles);
     }
-    bool any_split = false;
-    for (uint32_t k = ll.seg_begin; k < ll.seg_begin + ll.seg_count; ++k) any_split |= hp.segs[k].split != 0;
-    if (any_split) hp.split_items = std::max<uint64_t>(hp.split_items, ll.seg_items);
   }
   for (int e : chunk_err) {
     if (e == 1) throw Error(kResource, "tensor rank exceeds the device limit " + std::to_string(kMaxRank));

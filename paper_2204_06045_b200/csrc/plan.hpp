@@ -39,10 +39,6 @@ struct HostPlan {
   // per lightcone: its slot in the multi-GPU reduce vector (the edge index;
   // build_plan sets 0..n-1, callers overwrite before the upload)
   std::vector<int32_t> lc_edge;
-  // split tiles: the largest seg_kernel item count of a level with split
-  // segments (sizes the device scratch: 2 rows x 32 lanes per item, and one
-  // arrival counter per item)
-  uint64_t split_items = 0;
   uint64_t input_elems = 0;
   uint64_t arena_elems = 0;            // peak arena size (elements)
   // accounting: B_alg = sum_in 16*2^rank + 16*2^r; ops = 2^width
