@@ -73,6 +73,47 @@ __device__ __forceinline__ V cadd(V a, V b) { return mkv(radd(a.x, b.x), radd(a.
 
 __device__ __forceinline__ V ld(const V* p) { return __ldg(p); }
 
+// ---- bulk async copy (cp.async.bulk + mbarrier; SASS UBLKCP / SYNCS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Stage `count` consecutive uint32 of global memory into shared memory with
+// ONE bulk copy issued by thread 0, completion tracked by the mbarrier `bar`
+// (initialised here; single use).  The copy is widened to 16-byte alignment
+// on both ends: the returned skew is where src[0] landed (dst[skew + i] ==
+// src[i]); dst must hold count + 7 words; the up to 12 bytes read past the
+// end must be readable (the descriptor blob's 256-byte padding).  Every
+// thread of the CTA must call this (it contains __syncthreads).
+__device__ __forceinline__ uint32_t bulk_stage_u32(uint32_t* dst, const uint32_t* src,
+                                                   uint32_t count, uint64_t* bar) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const uint32_t skew = static_cast<uint32_t>((a & 15u) >> 2);
+  const uint32_t nbytes = ((count + skew + 3u) & ~3u) * 4u;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(nbytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(a & ~uintptr_t{15}), "r"(nbytes), "r"(smem_u32(bar))
+        : "memory");
+  }
+  __syncthreads();
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar))
+        : "memory");
+  return skew;
+}
+
 // Product over the T operands of one summed assignment (left fold, member order).
 template <int T>
 __device__ __forceinline__ V chain(const V* const* base, const uint32_t* off,
@@ -253,13 +294,14 @@ level_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
   return;
 #endif
   __shared__ DevTensor slots[kWarpsPerCta][MAXT];
-  __shared__ uint32_t sbeg[kSmemOps];
-  // cache the item table in shared memory (the cooperative copy costs one
+  __shared__ alignas(16) uint32_t sbeg_raw[kSmemOps + 8];
+  __shared__ alignas(8) uint64_t sbar;
+  // stage the item table in shared memory with one bulk async copy (one
   // round trip; a binary search in global memory costs ~12 dependent ones)
   const bool cached = op_count <= kSmemOps && items >= QTNG_LEVEL_CACHE_MIN * gridDim.x * kWarpsPerCta;
-  if (cached)
-    for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
-  __syncthreads();
+  const uint32_t* sbeg = sbeg_raw;
+  if (cached) sbeg = sbeg_raw + bulk_stage_u32(sbeg_raw, ibeg, op_count, &sbar);
+  else __syncthreads();
   const int lane = threadIdx.x & 31;
   DevTensor* slot = slots[threadIdx.x >> 5];
   const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -383,13 +425,13 @@ outer_kernel(const DevOp* __restrict__ ops, const uint32_t* __restrict__ ibeg,
   return;
 #endif
   __shared__ DevTensor slots[kWarpsPerCta][4];
-  __shared__ uint32_t sbeg[kSmemOps];
-  // cache the item table in shared memory (the cooperative copy costs one
-  // round trip; a binary search in global memory costs ~12 dependent ones)
+  __shared__ alignas(16) uint32_t sbeg_raw[kSmemOps + 8];
+  __shared__ alignas(8) uint64_t sbar;
+  // the item table staged in shared memory by one bulk async copy
   const bool cached = op_count <= kSmemOps && items >= QTNG_LEVEL_CACHE_MIN * gridDim.x * kWarpsPerCta;
-  if (cached)
-    for (uint32_t i = threadIdx.x; i < op_count; i += kThreads) sbeg[i] = __ldg(ibeg + i);
-  __syncthreads();
+  const uint32_t* sbeg = sbeg_raw;
+  if (cached) sbeg = sbeg_raw + bulk_stage_u32(sbeg_raw, ibeg, op_count, &sbar);
+  else __syncthreads();
   const int lane = threadIdx.x & 31;
   DevTensor* slot = slots[threadIdx.x >> 5];
   const uint32_t warp = (blockIdx.x * kThreads + threadIdx.x) >> 5;
