@@ -61,18 +61,19 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def committed_traffic(kernel):
-    """DRAM read+write bytes per step of `kernel`, from the newest committed
-    ncu launch list (profiles/<tag>/traffic.json, written by
-    tools/summarize_profiles.py) -- ncu numbers are never measured here."""
+def committed_traffic(*kernels):
+    """DRAM read+write bytes per step of `kernels` (summed), from the newest
+    committed ncu launch list (profiles/<tag>/traffic.json, written by
+    tools/summarize_profiles.py; tags sort by round and letter) -- ncu numbers
+    are never measured here."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")),
-                   key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")))
     for fn in reversed(files):
         with open(fn) as f:
             t = json.load(f)
-        if kernel in t.get("dram_bytes_per_step", {}):
-            return {"traffic": t["dram_bytes_per_step"][kernel], "traffic_source": t["source"]}
+        per = t.get("dram_bytes_per_step", {})
+        if kernels[0] in per:
+            return {"traffic": sum(per.get(k, 0.0) for k in kernels), "traffic_source": t["source"]}
     return {"traffic": None}
 
 
@@ -414,7 +415,7 @@ def run_b200(args, cfg):
                                       f"derived: {sms} SMs x 64 FP64 lanes x sm_max_mhz")),
                      "peak_derived": fp_peak_derived / 1e12,
                      "peak_fma_tflops_measured": (mpk_fma / 1e12) if mpk_fma else None,
-                     **committed_traffic("seg_kernel"),
+                     **committed_traffic("seg_kernel", "seg4_kernel"),
                      "flops_per_step": info.seg_fp64_ops,
                      "flops_def": "the reference NaiveBackend loop's FP64 mul+add count of the "
                                   "buckets the fused-chain kernels evaluate",
