@@ -446,13 +446,22 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   auto seg_cost = [&](uint32_t u) {
     return (uint64_t{1} << (unit_len[u] - 1)) * (unit_nops[u] + op_at(unit_first[u]).nin);
   };
-  for (int L = 0; L < n_levels; ++L)
-    std::stable_sort(order.begin() + lstart[L], order.begin() + lstart[L + 1],
-                     [&](uint32_t a, uint32_t b) {
-                       const int ga = group_of(a), gb = group_of(b);
-                       if (ga != gb) return ga < gb;
-                       return ga == 2 && seg_cost(a) > seg_cost(b);
-                     });
+  Pool::get().parallel_for(n_levels, [&](int L) {
+    // sort keys first: the comparator would chase op pointers O(n log n) times
+    const uint32_t n = lstart[L + 1] - lstart[L];
+    std::vector<std::pair<uint64_t, uint32_t>> key(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t u = order[lstart[L] + i];
+      const int gr = group_of(u);
+      // group ascending, then (segments) cost descending, then stable
+      const uint64_t cost = gr == 2 ? seg_cost(u) : 0;
+      key[i] = {(static_cast<uint64_t>(gr) << 56) | ((~cost) & ((uint64_t{1} << 56) - 1)), i};
+    }
+    std::sort(key.begin(), key.end());
+    std::vector<uint32_t> tmp(n);
+    for (uint32_t i = 0; i < n; ++i) tmp[i] = order[lstart[L] + key[i].second];
+    std::copy(tmp.begin(), tmp.end(), order.begin() + lstart[L]);
+  });
 
   ptm.mark("outer+order");
   // descriptors, level by level: item/tref prefix sums sequentially ...
@@ -796,6 +805,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     for (uint32_t u = 0; u < U; ++u)
       if (unit_len[u] > 1) unit_slot[u] = slot_of[unit_slot[u]];
   }
+  ptm.mark("seg re-sort");
   for (LevelLaunch& ll : hp.levels) {
     ll.seg_items = 0;
     ll.seg4_items = 0;
@@ -813,26 +823,56 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     if (e == 2) throw Error(kSchedule, "internal: operand var outside its bucket");
     if (e == 3) throw Error(kSchedule, "internal: operand reads a fused intermediate");
   }
-  for (uint32_t u = 0; u < U; ++u) {
-    const int L = unit_level[u];
-    hp.dev_bytes += unit_dev_bytes[u];
-    if (unit_len[u] > 1) hp.n_fused_ops += unit_len[u];
-    for (uint32_t g = unit_first[u]; g != ~0u; g = next_in_unit[g]) {
-      const Op& o = op_at(g);
-      hp.level_bytes[L] += op_bytes[g];
-      hp.alg_bytes += op_bytes[g];
-      // the reference's FP64 operations (NaiveBackend::contract): per summed
-      // assignment nt-1 complex products (4 mul + 2 add/sub), per output
-      // 2^ns - 1 complex additions
-      const double fl = 6.0 * std::ldexp(1.0, o.width) * (o.nin - 1) +
-                        2.0 * std::ldexp(1.0, o.r) * (std::ldexp(1.0, o.ns) - 1.0);
-      hp.fp64_ops += fl;
-      if (unit_len[u] > 1) hp.seg_fp64_ops += fl; else hp.single_alg_bytes += op_bytes[g];
-      if (o.bucket_seq >= 0) {
-        hp.sum_ops += static_cast<double>(uint64_t{1} << o.width);
-        ++hp.n_buckets;
-        hp.max_width = std::max(hp.max_width, static_cast<int>(o.width));
+  ptm.mark("items");
+  // accounting (statistics only), in parallel over unit chunks
+  {
+    struct Acc {
+      double dev = 0, alg = 0, fp = 0, segfp = 0, single = 0, sum_ops = 0;
+      uint64_t fused = 0, buckets = 0;
+      int max_width = 0;
+      std::vector<double> level_bytes;
+    };
+    const int nch = std::max(1, std::min<int>(Pool::get().size() * 2, static_cast<int>(U / 256) + 1));
+    std::vector<Acc> acc(nch);
+    Pool::get().parallel_for(nch, [&](int ch) {
+      Acc& a = acc[ch];
+      a.level_bytes.assign(n_levels, 0.0);
+      const uint32_t u0 = static_cast<uint32_t>(uint64_t{U} * ch / nch);
+      const uint32_t u1 = static_cast<uint32_t>(uint64_t{U} * (ch + 1) / nch);
+      for (uint32_t u = u0; u < u1; ++u) {
+        const int L = unit_level[u];
+        a.dev += unit_dev_bytes[u];
+        if (unit_len[u] > 1) a.fused += unit_len[u];
+        for (uint32_t g = unit_first[u]; g != ~0u; g = next_in_unit[g]) {
+          const Op& o = op_at(g);
+          a.level_bytes[L] += op_bytes[g];
+          a.alg += op_bytes[g];
+          // the reference's FP64 operations (NaiveBackend::contract): per summed
+          // assignment nt-1 complex products (4 mul + 2 add/sub), per output
+          // 2^ns - 1 complex additions
+          const double fl = 6.0 * std::ldexp(1.0, o.width) * (o.nin - 1) +
+                            2.0 * std::ldexp(1.0, o.r) * (std::ldexp(1.0, o.ns) - 1.0);
+          a.fp += fl;
+          if (unit_len[u] > 1) a.segfp += fl; else a.single += op_bytes[g];
+          if (o.bucket_seq >= 0) {
+            a.sum_ops += static_cast<double>(uint64_t{1} << o.width);
+            ++a.buckets;
+            a.max_width = std::max(a.max_width, static_cast<int>(o.width));
+          }
+        }
       }
+    });
+    for (const Acc& a : acc) {
+      hp.dev_bytes += a.dev;
+      hp.n_fused_ops += a.fused;
+      hp.alg_bytes += a.alg;
+      hp.fp64_ops += a.fp;
+      hp.seg_fp64_ops += a.segfp;
+      hp.single_alg_bytes += a.single;
+      hp.sum_ops += a.sum_ops;
+      hp.n_buckets += a.buckets;
+      hp.max_width = std::max(hp.max_width, a.max_width);
+      for (int L = 0; L < n_levels; ++L) hp.level_bytes[L] += a.level_bytes[L];
     }
   }
 
@@ -886,27 +926,41 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   }
 
   ptm.mark("accounting");
-  // records (one per non-empty bucket, walk order) and per-lightcone scalars
-  hp.rec_begin.reserve(C + 1);
-  hp.rec_begin.push_back(0);
-  hp.lc_begin.reserve(C + 1);
-  hp.lc_begin.push_back(0);
+  // records (one per non-empty bucket, walk order) and per-lightcone scalars:
+  // offsets first, then every lightcone fills its own range in parallel
+  hp.rec_begin.assign(C + 1, 0);
+  hp.lc_begin.assign(C + 1, 0);
   for (int c = 0; c < C; ++c) {
     const WalkResult& w = *cones[c];
+    uint32_t nrec = 0;
+    for (const Op& o : w.ops) nrec += o.bucket_seq >= 0;
+    hp.rec_begin[c + 1] = hp.rec_begin[c] + nrec;
+    hp.lc_begin[c + 1] = hp.lc_begin[c] + static_cast<uint32_t>(w.scalars.size());
+    hp.lc_edge.push_back(c);
+  }
+  const uint32_t R = hp.rec_begin[C];
+  hp.rec_seq.resize(R);
+  hp.rec_width.resize(R);
+  hp.rec_level.resize(R);
+  hp.rec_bytes.resize(R);
+  hp.rec_out.resize(R);
+  hp.scalar_off.resize(hp.lc_begin[C]);
+  Pool::get().parallel_for(C, [&](int c) {
+    const WalkResult& w = *cones[c];
+    uint32_t r = hp.rec_begin[c];
     for (uint32_t k = 0; k < w.ops.size(); ++k) {
       const Op& o = w.ops[k];
       if (o.bucket_seq < 0) continue;
-      hp.rec_seq.push_back(o.bucket_seq);
-      hp.rec_width.push_back(o.width);
-      hp.rec_level.push_back(level_of(base[c] + k));
-      hp.rec_bytes.push_back(op_bytes[base[c] + k]);
-      hp.rec_out.push_back(out[base[c] + k]);
+      hp.rec_seq[r] = o.bucket_seq;
+      hp.rec_width[r] = o.width;
+      hp.rec_level[r] = level_of(base[c] + k);
+      hp.rec_bytes[r] = op_bytes[base[c] + k];
+      hp.rec_out[r] = out[base[c] + k];
+      ++r;
     }
-    hp.rec_begin.push_back(static_cast<uint32_t>(hp.rec_seq.size()));
-    for (int s : w.scalars) hp.scalar_off.push_back(out[base[c] + s]);
-    hp.lc_begin.push_back(static_cast<uint32_t>(hp.scalar_off.size()));
-    hp.lc_edge.push_back(c);
-  }
+    uint32_t q = hp.lc_begin[c];
+    for (int sc : w.scalars) hp.scalar_off[q++] = out[base[c] + sc];
+  });
   ptm.mark("records");
   return hp;
 }
