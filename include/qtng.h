@@ -142,6 +142,15 @@ qtng_status qtng_edge_schedule(int n, int m, const int* edges, int p, const doub
                                int64_t int_cap, double* data, int64_t data_cap,
                                int64_t* n_ints, int64_t* n_data, int* n_buckets, int* merges);
 
+/* merge_buckets (proj/src/engine.cpp:306-358) of an explicit schedule (format
+ * of qtng_edge_schedule; tensor data is not needed).  Output per merged
+ * bucket: n_sum, sum vars, n_tensors, then each member's index among the
+ * input schedule's tensors (flattened order), so the caller moves its own
+ * tensors.  *n_out / *out_buckets: sizes (nothing written when cap is
+ * short); merges (may be NULL): merges_applied, merges_skipped.  Host only. */
+qtng_status qtng_merge_schedule(int n_buckets, const int* ints, int64_t n_ints, int* out,
+                                int64_t cap, int64_t* n_out, int* out_buckets, int* merges);
+
 /* simulate_widths (proj/src/engine.cpp:235-240) of one edge's schedule. */
 qtng_status qtng_simulate_widths(int n, int m, const int* edges, int p, int edge_index,
                                  int merged, int* widths, int cap, int* n_out);

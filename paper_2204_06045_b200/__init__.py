@@ -419,6 +419,32 @@ def _parse_flat(ints, data, n_buckets) -> ContractionSchedule:
     return ContractionSchedule(buckets)
 
 
+def merge_buckets(schedule: ContractionSchedule) -> ContractionSchedule:
+    """merge_buckets (engine.cpp:306-358) of an explicit schedule: bucket A is
+    folded into the first later bucket covering its kept vars when the
+    schedule stays valid and no bucket grows past the widest one.  Tensors
+    are moved, not copied; merges_applied / merges_skipped as the reference
+    counts them."""
+    ints, n_ints, _ = schedule.flatten()
+    tensors = [t for b in schedule.buckets for t in b.tensors]
+    n_out, nb = C.c_int64(0), C.c_int(0)
+    merges = np.zeros(2, np.int32)
+    _check(lib.qtng_merge_schedule(len(schedule.buckets), ints, n_ints, None, 0, C.byref(n_out),
+                                   C.byref(nb), None))
+    out = np.zeros(max(1, n_out.value), np.int32)
+    _check(lib.qtng_merge_schedule(len(schedule.buckets), ints, n_ints,
+                                   out.ctypes.data_as(C.c_void_p), len(out), C.byref(n_out),
+                                   C.byref(nb), merges.ctypes.data_as(C.c_void_p)))
+    buckets, i = [], 0
+    for _ in range(nb.value):
+        ns = int(out[i]); i += 1
+        sums = [int(x) for x in out[i:i + ns]]; i += ns
+        nt = int(out[i]); i += 1
+        buckets.append(Bucket(sums, [tensors[int(k)] for k in out[i:i + nt]]))
+        i += nt
+    return ContractionSchedule(buckets, int(merges[0]), int(merges[1]))
+
+
 def simulate_widths(g: Graph, edge_index: int, p: int, merged: bool = False) -> List[int]:
     """simulate_widths (engine.cpp:235-240) of one edge's schedule."""
     buf = np.zeros(1 << 16, dtype=np.int32)

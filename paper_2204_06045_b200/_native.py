@@ -88,6 +88,8 @@ def _load():
     lib.qtng_plan_create.argtypes = [vp, C.c_int, C.c_int, i32p, C.c_int, C.c_int, C.c_int,
                                      C.c_int, C.c_int, C.c_void_p, pvp]
     lib.qtng_plan_terms.argtypes = [vp, f64p]
+    lib.qtng_merge_schedule.argtypes = [C.c_int, i32p, C.c_int64, C.c_void_p, C.c_int64,
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_int), C.c_void_p]
     lib.qtng_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.qtng_plan_create_schedule.argtypes = [vp, C.c_int, i32p, C.c_int64, f64p, C.c_int, pvp]
     lib.qtng_plan_execute.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -121,7 +123,7 @@ lib = _load()
 EXPORTED = [
     "qtng_create", "qtng_destroy", "qtng_last_error", "qtng_version", "qtng_random_regular",
     "qtng_edge_schedule", "qtng_simulate_widths", "qtng_edge_costs", "qtng_edge_work", "qtng_validate_energy", "qtng_plan_dump", "qtng_contract_bucket",
-    "qtng_contract_schedule", "qtng_energy", "qtng_energy_multi", "qtng_shard_edges", "qtng_plan_terms", "qtng_fp64_peak", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute", "qtng_plan_profile",
+    "qtng_contract_schedule", "qtng_energy", "qtng_energy_multi", "qtng_shard_edges", "qtng_plan_terms", "qtng_merge_schedule", "qtng_fp64_peak", "qtng_plan_create", "qtng_plan_create_schedule", "qtng_plan_execute", "qtng_plan_profile",
     "qtng_plan_run_device", "qtng_plan_info_get", "qtng_plan_stats", "qtng_kernel_launches", "qtng_set_precision", "qtng_statevector_energy", "qtng_plan_segments", "qtng_plan_records", "qtng_plan_level_ms", "qtng_plan_kernel_ms",
     "qtng_plan_destroy", "qtng_plan_time_level",
 ]

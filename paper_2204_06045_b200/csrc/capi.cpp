@@ -677,6 +677,28 @@ qtng_status qtng_edge_schedule(int n, int m, const int* edges, int p, const doub
   });
 }
 
+qtng_status qtng_merge_schedule(int n_buckets, const int* ints, int64_t n_ints, int* out,
+                                int64_t cap, int64_t* n_out, int* out_buckets, int* merges) {
+  return guarded([&] {
+    if (!n_out || !out_buckets) throw Error(kInvalidInput, "null argument");
+    const Schedule s = merge_buckets(parse_schedule(n_buckets, ints, static_cast<long>(n_ints)));
+    std::vector<int> v;
+    for (const SchedBucket& b : s.buckets) {
+      v.push_back(static_cast<int>(b.sum_vars.size()));
+      v.insert(v.end(), b.sum_vars.begin(), b.sum_vars.end());
+      v.push_back(static_cast<int>(b.tensors.size()));
+      v.insert(v.end(), b.tensors.begin(), b.tensors.end());  // input tensor indices
+    }
+    *n_out = static_cast<int64_t>(v.size());
+    *out_buckets = static_cast<int>(s.buckets.size());
+    if (merges) {
+      merges[0] = s.merges_applied;
+      merges[1] = s.merges_skipped;
+    }
+    if (out && static_cast<int64_t>(v.size()) <= cap) std::copy(v.begin(), v.end(), out);
+  });
+}
+
 qtng_status qtng_simulate_widths(int n, int m, const int* edges, int p, int edge_index,
                                  int merged, int* widths, int cap, int* n_out) {
   return guarded([&] {

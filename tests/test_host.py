@@ -211,3 +211,49 @@ def test_lpt_shards_on_predicted_work(q, golden):
         assert loads.max() <= loads.mean() + w.max() + 1e-6
         assert np.array_equal(own, q.shard_edges(g, 4, k))
     assert (q.shard_edges(g, 4, 1) == 0).all()
+
+
+def _sched(q, buckets):
+    return q.ContractionSchedule([q.Bucket(s, [q.Tensor(f"t{i}_{k}", v, np.asarray(d, complex))
+                                               for k, (v, d) in enumerate(ts)])
+                                  for i, (s, ts) in enumerate(buckets)])
+
+
+def test_merge_nested_var_sets_collapse(q):
+    # test_engine.cpp:173-195
+    r = 1.0 / np.sqrt(2.0)
+    s = _sched(q, [([0], [([0, 1], [r, 0, 0, r])]), ([1], [([1, 2], [1, 0, 0, 1])]),
+                   ([2], [([2], [1, 1])])])
+    m = q.merge_buckets(s)
+    assert len(m.buckets) < len(s.buckets) and m.merges_applied >= 1
+
+
+def test_merge_blocked_by_non_nested_kept_vars(q):
+    # test_engine.cpp:197-218: bucket 0 keeps {3,4}; no single later bucket covers both
+    s = _sched(q, [([0], [([0, 3, 4], [1] * 8)]), ([3], [([3], [3, 4])]), ([4], [([4], [1, 2])])])
+    m = q.merge_buckets(s)
+    assert len(m.buckets[0].tensors) == 1 and m.buckets[0].tensors[0].label == "t0_0"
+    assert m.buckets[0].sum_vars == [0]
+
+
+def test_merge_unrelated_buckets_not_chained(q):
+    # test_engine.cpp:220-234
+    s = _sched(q, [([0], [([0], [1, 2])]), ([1], [([1], [3, 4])])])
+    m = q.merge_buckets(s)
+    assert len(m.buckets) == 2 and m.merges_applied == 0
+
+
+def test_merge_explicit_equals_edge_schedule_merge(q):
+    """merge_buckets on an unmerged edge schedule == edge_schedule(merged=True)."""
+    g = q.random_regular(10, 3, 13)
+    a = q.Angles([0.6, 0.2], [0.1, 0.5])
+    for i in range(g.m):
+        m = q.merge_buckets(q.edge_schedule(g, i, a))
+        e = q.edge_schedule(g, i, a, merged=True)
+        assert [(b.sum_vars, [t.vars for t in b.tensors]) for b in m.buckets] == \
+            [(b.sum_vars, [t.vars for t in b.tensors]) for b in e.buckets]
+        assert (m.merges_applied, m.merges_skipped) == (e.merges_applied, e.merges_skipped)
+        # test_engine.cpp:265-273: merged buckets are at least as wide as their sums
+        for b in m.buckets:
+            if len(b.sum_vars) > 1:
+                assert len({v for t in b.tensors for v in t.vars}) >= len(b.sum_vars)
