@@ -79,7 +79,12 @@ static_assert(sizeof(DevTensor) == 48, "DevTensor layout");
 //   32..63   tile-number bit (code - 32 = Y bit - cY)
 //   64       stage 1's own summed bit (stage 1 sums at most one var)
 constexpr int kSegYBits = 5;         // cY = min(rY, kSegYBits)
-constexpr int kSegMaxJ = 5;          // digits per segment (dlo/dhi tables: 4 + 1 bits)
+#ifndef QTNG_SEG_MAXJ
+#define QTNG_SEG_MAXJ 4
+#endif
+// digits per segment (dlo/dhi tables: 4 + 1 bits).  4: the per-warp climb
+// state shrinks by 1 KB, which leaves the L1 data cache 32 KB more per SM
+constexpr int kSegMaxJ = QTNG_SEG_MAXJ;
 constexpr int kSegMaxStages = kSegMaxJ + 1;
 constexpr int kSegMaxOps = 16;       // operands per segment (all stages)
 constexpr int kSegMaxNt1 = 6;        // members of stage 1

@@ -51,7 +51,10 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarpsPerCta = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kSmemOps = 4096;  // item_begin entries cached in shared memory
+#ifndef QTNG_SMEM_OPS
+#define QTNG_SMEM_OPS 4096
+#endif
+constexpr int kSmemOps = QTNG_SMEM_OPS;  // item_begin entries staged in shared memory
 #ifndef QTNG_LEVEL_CACHE_MIN
 #define QTNG_LEVEL_CACHE_MIN 0u  // items per warp from which a CTA caches the item table (tuned)
 #endif
