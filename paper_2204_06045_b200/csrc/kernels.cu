@@ -1438,7 +1438,7 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
 }
 
 #ifndef QTNG_SEG4_MINB
-#define QTNG_SEG4_MINB 16  // resident seg4_kernel warps per SM the register budget must allow (128 regs)
+#define QTNG_SEG4_MINB 20  // resident seg4_kernel warps per SM the register budget must allow (96 regs; measured: 16 -> 2.206, 20 -> 2.151, 24 -> 2.149 ms)
 #endif
 __global__ void __launch_bounds__(32, QTNG_SEG4_MINB)
 seg4_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
