@@ -525,12 +525,12 @@ struct ChainWarp {
   uint32_t toff[kSegMaxOps];             // tile part of each operand's offset
   DevStage st[kSegMaxStages];
   V ptab[kSegMaxStages - 1][8];    // [i - 1]: tabulated side products P_i(s_i, u0, u1) of this tile
-  uint8_t preal[kSegMaxStages];          // 1: P_i is a real scalar (scale instead of multiply)
   // per stage: bits 0-1 mode (0 no side member, 1 table, 2 real table, 3
-  // gathered), bits 8-12 / 13 and 16-20 / 21: digit position / valid of the
-  // table index bits 1 and 2
+  // gathered), bits 8-12 / 13 and 16-20 / 21: source position / valid of the
+  // table index bits 1 and 2, a position in x = j | lane << 16 (a digit bit
+  // of j, or 16 + a lane bit); no per-lane table, so the climb state stays
+  // small enough for the SM's 132 KB carveout (more L1)
   uint32_t sdesc[kSegMaxStages];
-  uint8_t slane[kSegMaxStages - 1][32];  // [i - 1], per lane: the lane bits of the table index
   V acc[kSegMaxStages - 2][32];    // per lane: parked s_i = 0 terms of stage k + 2 (k >= 1)
   V acc1[kSegMaxStages - 2][32];   // ... of the second row (paired segments)
   uint32_t drow[kSegMaxNt1];       // paired: stage-1 member offset of the second row
@@ -593,9 +593,9 @@ __device__ __forceinline__ V chain_term(const ChainWarp& cw, const SegOpTab* __r
   const uint32_t mode = d & 3u;
   if (mode == 0) return v;
   if (mode != 3) {
-    const uint32_t idx = cw.slane[k][lane] | ((j >> k) & 1u) |
-                         (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
-                         (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
+    const uint32_t x = j | (static_cast<uint32_t>(lane) << 16);
+    const uint32_t idx = ((j >> k) & 1u) | (((x >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
+                         (((x >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
     const V p = cw.ptab[k][idx];
     return mode == 2 ? rscale(p.x, v) : cmul(p, v);
   }
@@ -616,9 +616,9 @@ __device__ __forceinline__ void chain_term2(const ChainWarp& cw, const SegOpTab*
   V p;
   bool real;
   if (mode != 3) {
-    const uint32_t idx = cw.slane[k][lane] | ((j >> k) & 1u) |
-                         (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
-                         (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
+    const uint32_t x = j | (static_cast<uint32_t>(lane) << 16);
+    const uint32_t idx = ((j >> k) & 1u) | (((x >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
+                         (((x >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
     p = cw.ptab[k][idx];
     real = mode == 2;
   } else {
@@ -1058,7 +1058,6 @@ __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const D
     bool real = lane > 0 && st.nt > 1;  // every side member a real scalar
     for (int t = 0; real && t < st.nt - 1; ++t)
       real = __ldg(&segtab[sg.tref + st.op0 + t].kind) == kTensorRealScalar;
-    cw.preal[lane] = real ? 1 : 0;
     for (int w = 0; w < 2; ++w)  // quad rows' bits are table index bits, not tile values
       tile_dep |= st.ptab && st.u[w] >= kTileSrc && st.u[w] < kSumSrc &&
                   !(quad && (st.u[w] == kTileSrc + sg.rb || st.u[w] == kTileSrc + sg.rb2));
@@ -1067,18 +1066,12 @@ __device__ __forceinline__ void seg_switch(ChainWarp& cw, SegCursor& sc, const D
     for (int w = 0; w < 2; ++w)
       if (mode == 1u || mode == 2u) {
         const uint32_t c = st.u[w];
-        if (c >= kJSrc && c < kTileSrc) d |= ((c - kJSrc) | 32u) << (8 + 8 * w);
+        if (c >= kJSrc && c < kTileSrc) d |= ((c - kJSrc) | 32u) << (8 + 8 * w);   // digit bit of j
+        else if (c < kLaneSrcEnd) d |= ((16u + c) | 32u) << (8 + 8 * w);        // lane bit
       }
     cw.sdesc[lane] = d;
   }
   __syncwarp();
-  for (int i = 1; i < sg.nst; ++i) {  // lane bits of each table index
-    const DevStage st = cw.st[i];
-    uint32_t b = 0;
-    for (int w = 0; w < 2; ++w)
-      if (st.u[w] < kLaneSrcEnd) b |= ((static_cast<uint32_t>(lane) >> st.u[w]) & 1u) << (1 + w);
-    cw.slane[i - 1][lane] = static_cast<uint8_t>(b);
-  }
   // the side-product tables depend on the tile only through tile-bit u's
   sc.ptab_tile = __any_sync(kFull, tile_dep);
   sc.ptab_fresh = false;
@@ -1186,9 +1179,9 @@ __device__ __forceinline__ void chain_term4(const ChainWarp4& cw, const SegOpTab
   if (mode == 0) return;
   const uint32_t rd = cw.rdesc[k + 1];
   if (mode != 3) {
-    const uint32_t idx = cw.b.slane[k][lane] | ((j >> k) & 1u) |
-                         (((j >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
-                         (((j >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
+    const uint32_t jx = j | (static_cast<uint32_t>(lane) << 16);
+    const uint32_t idx = ((j >> k) & 1u) | (((jx >> ((d >> 8) & 31u)) & (d >> 13) & 1u) << 1) |
+                         (((jx >> ((d >> 16) & 31u)) & (d >> 21) & 1u) << 2);
     const uint32_t ma = rd & 0xffu, mb = (rd >> 8) & 0xffu;
     if (!(ma | mb)) {
       const V p = cw.b.ptab[k][idx];
