@@ -62,3 +62,21 @@ def test_peak_tensor_bytes_bounded_by_widest_bucket(q, ctx):
     rep = q.contract_network(q.edge_schedule(g, 0, q.Angles([0.9], [0.2])), q.GpuBackend(ctx))
     w = max(r.width for r in rep.records)
     assert 16 <= rep.peak_tensor_bytes <= 16 * (1 << w)
+
+
+def test_small_and_degenerate_graphs(q, ctx):
+    """Edge cases the reference accepts: one edge, a path, a disconnected
+    graph (lightcones of separate components), and no edges at all; every
+    energy equals the device state-vector oracle, and an edgeless graph has
+    energy 0 (engine.cpp:549-560 with m = 0)."""
+    a = q.Angles([0.7, 0.2], [0.4, 0.9])
+    for n, edges in ((2, [(0, 1)]), (4, [(0, 1), (1, 2), (2, 3)]),
+                     (6, [(0, 1), (1, 2), (0, 2), (3, 4), (4, 5), (3, 5)])):
+        g = q.make_graph(n, edges)
+        res = q.energy_expectation(g, a, q.GpuBackend(ctx))
+        e_sv, _ = q.statevector_energy(g, a, ctx=ctx)
+        assert abs(res.energy - e_sv) < 1e-12, (n, edges)
+        plan = q.Plan(g, 2, ctx=ctx)
+        assert np.array_equal(plan.execute(a), res.terms)
+    g0 = q.make_graph(3, [])
+    assert q.energy_expectation(g0, a, q.GpuBackend(ctx)).energy == 0.0
