@@ -283,6 +283,8 @@ struct qtng_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf sv_scratch;     // state-vector oracle: edge bits, per-edge sums, partials
   DevBuf multi_full;     // qtng_energy_multi: the 2m-double term vector NCCL reduces
+  PinBuf stg[2];         // chunked staging of large pageable host buffers (bucket drop-in)
+  cudaEvent_t stg_ev[2] = {nullptr, nullptr};
   static constexpr int kLanes = 4;
   Lane lane[kLanes];     // lane 0 aliases the fields above; lanes 1.. own theirs
   DevBuf arena_x[kLanes], desc_x[kLanes];
@@ -558,6 +560,8 @@ qtng_status qtng_create(int device, uint64_t arena_bytes, qtng_ctx** out) {
     l0.pin_desc = &ctx->pin_desc;
     l0.pin_in = &ctx->pin_in;
     l0.pin_out = &ctx->pin_out;
+    for (cudaEvent_t* ev : {&ctx->stg_ev[0], &ctx->stg_ev[1]})
+      QTNG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (int i = 0; i < qtng_ctx::kLanes; ++i) {
       for (cudaEvent_t* ev : {&ctx->lane[i].t0, &ctx->lane[i].t1}) QTNG_CUDA(cudaEventCreate(ev));
       QTNG_CUDA(cudaStreamCreateWithFlags(&ctx->lane[i].s4, cudaStreamNonBlocking));
@@ -612,7 +616,8 @@ void ctx_release(qtng_ctx* ctx) {
     for (cudaEvent_t e : {ctx->lane[i].t0, ctx->lane[i].t1, ctx->lane[i].join4})
       if (e) cudaEventDestroy(e);
   }
-  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev})
+  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->fork_ev, ctx->join_ev, ctx->join3_ev,
+                        ctx->stg_ev[0], ctx->stg_ev[1]})
     if (e) cudaEventDestroy(e);
   delete ctx;  // frees the arenas and staging buffers
   for (cudaStream_t st : streams)
@@ -801,16 +806,61 @@ namespace {
 
 // Run a single-"lightcone" program whose inputs are `input` (complex count
 // input_elems) and return the HostPlan (for record / output offsets).
+// Large pageable host <-> device copies on the context stream through two
+// pinned 8 MiB chunks: the host memcpy of one chunk overlaps the DMA of the
+// other (a pageable cudaMemcpy runs at a few GB/s; the per-bucket drop-in
+// moves every bucket's operands and result across PCIe).  d2h returns with
+// the data in dst (synchronous).
+constexpr size_t kStageChunk = size_t{8} << 20;
+
+void h2d_staged(qtng_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  for (int b = 0; b < 2; ++b) ctx->stg[b].ensure(kStageChunk);
+  size_t i = 0;
+  for (size_t off = 0; off < bytes; off += kStageChunk, ++i) {
+    const int b = static_cast<int>(i & 1);
+    if (i >= 2) QTNG_CUDA(cudaEventSynchronize(ctx->stg_ev[b]));  // chunk i-2's DMA is done
+    const size_t n = std::min(kStageChunk, bytes - off);
+    std::memcpy(ctx->stg[b].p, static_cast<const char*>(src) + off, n);
+    QTNG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ctx->stg[b].p, n,
+                              cudaMemcpyHostToDevice, ctx->stream));
+    QTNG_CUDA(cudaEventRecord(ctx->stg_ev[b], ctx->stream));
+  }
+}
+
+void d2h_staged(qtng_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  for (int b = 0; b < 2; ++b) ctx->stg[b].ensure(kStageChunk);
+  const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](size_t i) {
+    const int b = static_cast<int>(i & 1);
+    const size_t off = i * kStageChunk, n = std::min(kStageChunk, bytes - off);
+    QTNG_CUDA(cudaMemcpyAsync(ctx->stg[b].p, static_cast<const char*>(src) + off, n,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    QTNG_CUDA(cudaEventRecord(ctx->stg_ev[b], ctx->stream));
+  };
+  for (size_t i = 0; i < nch && i < 2; ++i) issue(i);
+  for (size_t i = 0; i < nch; ++i) {
+    const int b = static_cast<int>(i & 1);
+    QTNG_CUDA(cudaEventSynchronize(ctx->stg_ev[b]));
+    const size_t off = i * kStageChunk, n = std::min(kStageChunk, bytes - off);
+    std::memcpy(static_cast<char*>(dst) + off, ctx->stg[b].p, n);
+    if (i + 2 < nch) issue(i + 2);
+  }
+}
+
 void run_program_once(qtng_ctx* ctx, const HostPlan& hp, const double* input,
                       uint64_t input_elems, double2* terms_host) {
   const DescLayout L = layout_of(hp);
   const size_t eb = elem_bytes(hp);
   ctx->ensure_arena(std::max(hp.arena_elems, input_elems), eb);
   ctx->desc.ensure(L.total);
-  ctx->pin_in.ensure(std::max<uint64_t>(input_elems, 1) * eb);
-  stage_input(hp, input, input_elems, ctx->pin_in.p);
-  QTNG_CUDA(cudaMemcpyAsync(ctx->arena.p, ctx->pin_in.p, input_elems * eb, cudaMemcpyHostToDevice,
-                            ctx->stream));
+  if (!hp.c64 && input_elems * eb > kStageChunk) {  // large inputs: chunked, overlapped staging
+    h2d_staged(ctx, ctx->arena.p, input, input_elems * eb);
+  } else {
+    ctx->pin_in.ensure(std::max<uint64_t>(input_elems, 1) * eb);
+    stage_input(hp, input, input_elems, ctx->pin_in.p);
+    QTNG_CUDA(cudaMemcpyAsync(ctx->arena.p, ctx->pin_in.p, input_elems * eb, cudaMemcpyHostToDevice,
+                              ctx->stream));
+  }
   upload_desc(ctx, hp, L, static_cast<char*>(ctx->desc.p));
   DevProgram pr{static_cast<char*>(ctx->desc.p), L, hp.c64};
   enqueue_program(ctx, hp, pr, ctx->arena.p, nullptr);
@@ -862,10 +912,7 @@ qtng_status qtng_contract_bucket(qtng_ctx* ctx, int n_tensors, const int* ranks,
     std::lock_guard<std::mutex> lk(ctx->mu);
     QTNG_CUDA(cudaSetDevice(ctx->device));
     run_program_once(ctx, hp, data, static_cast<uint64_t>(dof), nullptr);
-    QTNG_CUDA(cudaMemcpyAsync(out_data, ctx->A() + hp.rec_out[0],
-                              (size_t{1} << r) * sizeof(double2), cudaMemcpyDeviceToHost,
-                              ctx->stream));
-    QTNG_CUDA(cudaStreamSynchronize(ctx->stream));
+    d2h_staged(ctx, out_data, ctx->A() + hp.rec_out[0], (size_t{1} << r) * sizeof(double2));
     *out_rank = r;
     for (int k = 0; k < r; ++k) out_vars[k] = w.ids[w.out_vars(op)[k]];
   });
