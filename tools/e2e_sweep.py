@@ -14,9 +14,10 @@ for _ in range(20):
     t0 = time.perf_counter(); r = q.energy_expectation(g, a, q.GpuBackend(ctx)); ts.append(time.perf_counter() - t0)
 ts.sort(); print("median ms %%.3f min %%.3f energy %%r" %% (1e3 * ts[10], 1e3 * ts[0], r.energy))
 ''' % ROOT
-for order in ("0", "1"):
-    for k in ("1", "2", "3", "4"):
-        out = subprocess.run([sys.executable, "-c", code],
-                             env=dict(os.environ, QTNG_PIPELINE=k, QTNG_PIPELINE_ORDER=order),
-                             capture_output=True, text=True, timeout=300)
-        print("order", order, "lanes", k, out.stdout.strip(), out.stderr[-200:], flush=True)
+sweep = [dict(QTNG_PIPELINE=k, QTNG_PIPELINE_ORDER=o) for o in ("0", "1") for k in ("1", "2", "3", "4")]
+if len(sys.argv) > 1 and sys.argv[1] == "pool":  # host pool sizes, 3 repetitions each
+    sweep = [dict(QTNG_POOL_THREADS=t) for t in ("16", "14", "12", "8") for _ in range(3)]
+for env in sweep:
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
+                         capture_output=True, text=True, timeout=300)
+    print(env, out.stdout.strip(), out.stderr[-200:], flush=True)
