@@ -317,7 +317,7 @@ def run_b200(args, cfg):
         # ---- e2e: public API with host inputs
         clocks.interval = float(os.environ.get("QTNG_BENCH_E2E_SAMPLE_S", "0.005"))
         l_value = q.kernel_launches() - launches0
-        for _ in range(max(1, args.warmup // 2)):
+        for _ in range(max(3, args.warmup)):
             q.energy_expectation(g, a, q.GpuBackend(ctx), edges=mine, cfg=ecfg)
         barrier()
         l_e2e0 = q.kernel_launches()
