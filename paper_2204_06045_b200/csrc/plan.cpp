@@ -107,6 +107,21 @@ int seg_max_j() {
   return j;
 }
 
+// Level assignment of the units (QTNG_LEVELS): 0 = as soon as possible
+// (1 + the deepest producer); 1 = each lightcone's ASAP levels shifted so all
+// lightcones end on the last level; 2 = as late as possible (a unit runs on
+// the level before its consumer; roots on the last level; default).
+// Measured (graph replay, 1x B200): C2 2.10 / 2.05 / 1.87 ms, C4 seed 9
+// 1.18 / 1.13 / 1.04 ms for modes 0 / 1 / 2 -- a late unit shares its level
+// with the other lightcones' late units instead of idling the SMs early.
+int level_mode() {
+  static const int m = [] {
+    const char* v = std::getenv("QTNG_LEVELS");
+    return v ? std::atoi(v) : 2;
+  }();
+  return m;
+}
+
 // Levels whose segments have fewer tiles than this put digits on lanes
 // (QTNG_SEG_STARVED, default 1024).
 // Segments of levels with at least this many tiles pair their rows
@@ -336,6 +351,23 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
     const Op& o = op_at(unit_last[u]);
     return o.consumer >= 0 ? static_cast<int64_t>(unit_of[base[lc_of[unit_last[u]]] + o.consumer]) : -1;
   };
+  if (level_mode() == 1) {
+    Pool::get().parallel_for(C, [&](int c) {
+      const int shift = max_level - cus[c].max_level;
+      for (uint32_t u = ubase[c]; u < ubase[c + 1]; ++u) unit_level[u] += shift;
+    });
+  } else if (level_mode() == 2) {
+    // a consumer's last op follows its producers' last ops: visiting units
+    // in descending order of their last op sees every consumer first
+    Pool::get().parallel_for(C, [&](int c) {
+      for (uint32_t k = static_cast<uint32_t>(cones[c]->ops.size()); k-- > 0;) {
+        const uint32_t g = base[c] + k, u = unit_of[g];
+        if (unit_last[u] != g) continue;
+        const int64_t cu = consumer_unit(u);
+        unit_level[u] = cu >= 0 ? unit_level[cu] - 1 : max_level;
+      }
+    });
+  }
 
   // stable counting sort of units by level; release lists by consumer level
   std::vector<uint32_t> lstart(n_levels + 1, 0), order(U);
