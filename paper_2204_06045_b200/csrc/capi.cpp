@@ -293,6 +293,7 @@ struct qtng_ctx {
   // 128 = complex128, 64 = complex64.  Read once per call (atomic).
   std::atomic<int> prec{128};
   std::atomic<int> refs{1};  // the owner + one per live plan (ctx_release)
+  std::unique_ptr<qtng::Worker> enq;  // one-shot energy: chunk enqueue thread (under mu)
 
   // arena of `elems` elements of `elem_bytes` (16: double2, 8: float2)
   void ensure_arena(uint64_t elems, size_t elem_bytes = sizeof(double2)) {
@@ -1542,6 +1543,15 @@ void energy_run(qtng_ctx* ctx, const Graph& g, int p, const double* gammas, cons
   std::vector<double> table;
   std::unique_lock<std::mutex> lk(ctx->mu, std::defer_lock);
   LaneGuard guard{ctx, 0};
+  // chunk c's upload + launches run on the context's enqueue thread while
+  // this thread plans chunk c + 1; every exit waits for it before the lane
+  // guard synchronises (declared after the guard: destroyed first)
+  struct EnqDrain {
+    qtng::Worker* w = nullptr;
+    ~EnqDrain() {
+      if (w) try { w->wait(); } catch (...) {}
+    }
+  } drain;
   for (int c = 0; c < K; ++c) {
     if (pos[c].empty()) continue;
     const bool pre = order_mode == 1 && K > 1;
@@ -1581,9 +1591,22 @@ void energy_run(qtng_ctx* ctx, const Graph& g, int p, const double* gammas, cons
       }
     }
     guard.n = c + 1;
-    enqueue_energy_chunk_timed(ctx, ctx->lane[c], c == 0, hps[c], table.data(), full);
+    if (K > 1) {
+      if (!ctx->enq) ctx->enq = std::make_unique<qtng::Worker>();
+      drain.w = ctx->enq.get();
+      const HostPlan* hp = &hps[c];
+      const double* tb = table.data();
+      drain.w->submit([ctx, c, hp, tb, full] {
+        QTNG_CUDA(cudaSetDevice(ctx->device));
+        enqueue_energy_chunk_timed(ctx, ctx->lane[c], c == 0, *hp, tb, full);
+      });
+    } else {
+      enqueue_energy_chunk_timed(ctx, ctx->lane[c], c == 0, hps[c], table.data(), full);
+    }
     tm.mark("upload+enqueue");
   }
+  if (drain.w) drain.w->wait();  // rethrows an enqueue failure
+  tm.mark("enqueue wait");
   std::vector<float> lane_ms(K, 0.f);
   int first = -1;
   for (int c = 0; c < K; ++c) {

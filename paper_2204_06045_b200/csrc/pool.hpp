@@ -7,6 +7,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdlib>
+#include <deque>
 #include <exception>
 #include <functional>
 #include <mutex>
@@ -120,6 +121,76 @@ class Pool {
   std::atomic<uint64_t> gen_{0};
   static constexpr int kSpin = 2000;  // yields before sleeping on the condition variable
   bool stop_ = false;
+};
+
+// One background thread running submitted tasks in order: the one-shot
+// energy enqueues chunk c (descriptor upload, kernel launches) on it while
+// the calling thread plans chunk c + 1 on the pool.
+class Worker {
+ public:
+  Worker() : t_([this] { loop(); }) {}
+  ~Worker() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    t_.join();
+  }
+  void submit(std::function<void()> f) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.push_back(std::move(f));
+    }
+    cv_.notify_all();
+  }
+  // Blocks until every submitted task has run; rethrows the first exception
+  // (tasks submitted after a failure are skipped).
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return q_.empty() && !running_; });
+    if (err_) {
+      std::exception_ptr e = err_;
+      err_ = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      std::function<void()> f;
+      bool skip = false;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+        if (q_.empty()) return;
+        f = std::move(q_.front());
+        q_.pop_front();
+        running_ = true;
+        skip = err_ != nullptr;
+      }
+      if (!skip) {
+        try {
+          f();
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu_);
+          if (!err_) err_ = std::current_exception();
+        }
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        running_ = false;
+      }
+      done_cv_.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::deque<std::function<void()>> q_;
+  std::exception_ptr err_;
+  bool running_ = false, stop_ = false;
+  std::thread t_;  // last: started after the members it uses
 };
 
 }  // namespace qtng

@@ -2,7 +2,7 @@
 """Host/device phase times of energy_expectation (QTNG_TIMING=1, tuning aid)."""
 import os
 import sys
-os.environ["QTNG_TIMING"] = "1"
+os.environ.setdefault("QTNG_TIMING", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2204_06045_b200 as q  # noqa: E402
 
