@@ -1529,9 +1529,25 @@ void energy_run(qtng_ctx* ctx, const Graph& g, int p, const double* gammas, cons
         ++c;
     }
   } else {
-    for (size_t i = 0; i < s.size(); ++i) {
-      pos[i % K].push_back(static_cast<int>(i));
-      part[i % K].push_back(s[i]);
+    // QTNG_PIPELINE_HEAD=f: the first chunk takes a fraction f of the
+    // lightcones (the device starts after planning it), the others share
+    // the rest; default 1/K.  Chunks interleave the selection.
+    static const double head = [] {
+      const char* v = std::getenv("QTNG_PIPELINE_HEAD");
+      return v ? std::atof(v) : 0.0;
+    }();
+    const size_t n = s.size();
+    size_t n0 = n / K;
+    if (head > 0.0 && K > 1)
+      n0 = std::clamp<size_t>(static_cast<size_t>(head * static_cast<double>(n) + 0.5), 1, n - (K - 1));
+    // chunk 0: every (n / n0)-th lightcone; the rest round-robin over 1..K-1
+    std::vector<char> in0(n, 0);
+    for (size_t k = 0; k < n0; ++k) in0[k * n / n0] = 1;
+    int r = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const int c = in0[i] ? 0 : (K > 1 ? 1 + (r++ % (K - 1)) : 0);
+      pos[c].push_back(static_cast<int>(i));
+      part[c].push_back(s[i]);
     }
   }
   std::vector<ConeSet> cs(K);

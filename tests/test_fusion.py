@@ -137,7 +137,7 @@ def test_fused_equals_unfused_bitwise(golden, name):
                 {"QTNG_SEG_QUAD": "0"}, {"QTNG_SEG_QUAD": "1"},
                 {"QTNG_SEG_QUAD": "1", "QTNG_SEG_J": "2"},
                 {"QTNG_SEG_QUAD": "0", "QTNG_SEG_PAIR": "0"},
-                {"QTNG_LEVELS": "0"}, {"QTNG_LEVELS": "1"}):
+                {"QTNG_LEVELS": "0"}, {"QTNG_LEVELS": "1"}, {"QTNG_SEG_STARVED": "1024"}):
         fused = _child_energy(name, env)
         assert fused["segments"] > 0
         assert fused["terms"] == plain["terms"], str(env)
