@@ -1529,23 +1529,41 @@ void energy_run(qtng_ctx* ctx, const Graph& g, int p, const double* gammas, cons
         ++c;
     }
   } else {
-    // QTNG_PIPELINE_HEAD=f: the first chunk takes a fraction f of the
-    // lightcones (the device starts after planning it), the others share
-    // the rest; default 1/K.  Chunks interleave the selection.
-    static const double head = [] {
-      const char* v = std::getenv("QTNG_PIPELINE_HEAD");
-      return v ? std::atof(v) : 0.0;
+    // QTNG_PIPELINE_SPLIT="f0,f1,...": chunk c takes a fraction f_c of the
+    // lightcones (default 1/K each), chunks interleaving the selection: the
+    // device starts once chunk 0 is planned, and the last chunk's own
+    // latency chain runs after the host has planned it.
+    static const std::vector<double> split = [] {
+      std::vector<double> f;
+      if (const char* v = std::getenv("QTNG_PIPELINE_SPLIT"))
+        for (const char* q = v; *q;) {
+          char* e = nullptr;
+          const double x = std::strtod(q, &e);
+          if (e == q) break;
+          f.push_back(x);
+          q = *e == ',' ? e + 1 : e;
+        }
+      return f;
     }();
     const size_t n = s.size();
-    size_t n0 = n / K;
-    if (head > 0.0 && K > 1)
-      n0 = std::clamp<size_t>(static_cast<size_t>(head * static_cast<double>(n) + 0.5), 1, n - (K - 1));
-    // chunk 0: every (n / n0)-th lightcone; the rest round-robin over 1..K-1
-    std::vector<char> in0(n, 0);
-    for (size_t k = 0; k < n0; ++k) in0[k * n / n0] = 1;
-    int r = 0;
+    std::vector<double> want(K, 1.0 / K);
+    if (static_cast<int>(split.size()) == K) {
+      double t = 0.0;
+      for (double x : split) t += std::max(x, 0.0);
+      if (t > 0.0)
+        for (int c = 0; c < K; ++c) want[c] = std::max(split[c], 0.0) / t;
+    }
+    // largest-deficit assignment in selection order: chunk c receives about
+    // want[c] * n lightcones, spread evenly over the selection
+    std::vector<double> got(K, 0.0);
     for (size_t i = 0; i < n; ++i) {
-      const int c = in0[i] ? 0 : (K > 1 ? 1 + (r++ % (K - 1)) : 0);
+      int c = 0;
+      double best = -1e300;
+      for (int k = 0; k < K; ++k) {
+        const double d = want[k] * static_cast<double>(i + 1) - got[k];
+        if (d > best + 1e-12) best = d, c = k;
+      }
+      got[c] += 1.0;
       pos[c].push_back(static_cast<int>(i));
       part[c].push_back(s[i]);
     }
@@ -1589,7 +1607,8 @@ void energy_run(qtng_ctx* ctx, const Graph& g, int p, const double* gammas, cons
     }
     tm.mark("schedules+walks");
     if (ok.empty()) continue;
-    hps[c] = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true);
+    hps[c] = build_plan(ok, static_cast<uint64_t>(n_gate_slots(p)) * kSlotElems, fuse_default(), true,
+                        flow_default(), /*stats=*/false, /*records=*/want_records);
     hps[c].c64 = prec == 64;
     for (size_t k = 0; k < okpos[c].size(); ++k) hps[c].lc_edge[k] = s[okpos[c][k]];
     tm.mark("build_plan");

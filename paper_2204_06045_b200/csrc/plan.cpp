@@ -236,7 +236,7 @@ bool fuse_default() {
 }
 
 HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems, bool fuse,
-                    bool qaoa_gates, bool flow) {
+                    bool qaoa_gates, bool flow, bool stats, bool records) {
   HostPlan hp;
   hp.input_elems = input_elems;
   const int C = static_cast<int>(cones.size());
@@ -858,7 +858,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   }
   ptm.mark("items");
   // accounting (statistics only), in parallel over unit chunks
-  {
+  if (stats) {
     struct Acc {
       double dev = 0, alg = 0, fp = 0, segfp = 0, single = 0, sum_ops = 0;
       uint64_t fused = 0, buckets = 0;
@@ -966,7 +966,8 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   for (int c = 0; c < C; ++c) {
     const WalkResult& w = *cones[c];
     uint32_t nrec = 0;
-    for (const Op& o : w.ops) nrec += o.bucket_seq >= 0;
+    if (records)
+      for (const Op& o : w.ops) nrec += o.bucket_seq >= 0;
     hp.rec_begin[c + 1] = hp.rec_begin[c] + nrec;
     hp.lc_begin[c + 1] = hp.lc_begin[c] + static_cast<uint32_t>(w.scalars.size());
     hp.lc_edge.push_back(c);
@@ -981,7 +982,7 @@ HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_
   Pool::get().parallel_for(C, [&](int c) {
     const WalkResult& w = *cones[c];
     uint32_t r = hp.rec_begin[c];
-    for (uint32_t k = 0; k < w.ops.size(); ++k) {
+    for (uint32_t k = 0; records && k < w.ops.size(); ++k) {
       const Op& o = w.ops[k];
       if (o.bucket_seq < 0) continue;
       hp.rec_seq[r] = o.bucket_seq;

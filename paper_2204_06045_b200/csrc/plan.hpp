@@ -68,8 +68,11 @@ bool flow_default();
 // initial operands are classified by gate slot (DevTensor::kind).
 // flow: build a dataflow program (no arena reuse: every unit's output gets its
 // own region, so no warp can hold a stale L1 line of it).
+// stats = false skips the statistics pass (PlanInfo bytes / FP64 work /
+// level bytes stay 0); records = false leaves the per-bucket records empty
+// (the one-shot energy without a report needs neither)
 HostPlan build_plan(const std::vector<const WalkResult*>& cones, uint64_t input_elems,
                     bool fuse = fuse_default(), bool qaoa_gates = false,
-                    bool flow = flow_default());
+                    bool flow = flow_default(), bool stats = true, bool records = true);
 
 }  // namespace qtng

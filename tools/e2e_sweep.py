@@ -15,9 +15,10 @@ for _ in range(20):
 ts.sort(); print("median ms %%.3f min %%.3f energy %%r" %% (1e3 * ts[10], 1e3 * ts[0], r.energy))
 ''' % ROOT
 sweep = [dict(QTNG_PIPELINE=k, QTNG_PIPELINE_ORDER=o) for o in ("0", "1") for k in ("1", "2", "3", "4")]
-if len(sys.argv) > 1 and sys.argv[1] == "head":  # first-chunk fraction x lanes
-    sweep = [dict(QTNG_PIPELINE=k, QTNG_PIPELINE_HEAD=h) for k in ("3", "4", "2")
-             for h in ("0.1", "0.15", "0.2", "0.25", "0.333")]
+if len(sys.argv) > 1 and sys.argv[1] == "split":  # chunk fractions, two passes
+    splits = [("3", "1,1,1"), ("3", "0.45,0.35,0.2"), ("3", "0.4,0.35,0.25"), ("3", "0.5,0.3,0.2"),
+              ("2", "0.6,0.4"), ("2", "0.7,0.3"), ("4", "0.35,0.3,0.2,0.15"), ("3", "0.3,0.35,0.35")]
+    sweep = [dict(QTNG_PIPELINE=k, QTNG_PIPELINE_SPLIT=f) for _ in range(2) for k, f in splits]
 if len(sys.argv) > 1 and sys.argv[1] == "pool":  # host pool sizes, 3 repetitions each
     sweep = [dict(QTNG_POOL_THREADS=t) for t in ("16", "14", "12", "8") for _ in range(3)]
 for env in sweep:
