@@ -1438,6 +1438,9 @@ seg4_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
             const DevStage* __restrict__ stages, const DevTensor* __restrict__ trefs,
             const SegOpTab* __restrict__ segtab, V* __restrict__ arena, uint32_t seg_count,
             uint32_t items, uint32_t* ctr) {
+#ifdef QTNG_NOOP_SEG  // launch-floor experiments only
+  return;
+#endif
   __shared__ ChainWarp4 cw;
   const int lane = threadIdx.x & 31;
   SegCursor sc;
