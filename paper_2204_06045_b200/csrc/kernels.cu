@@ -1431,7 +1431,11 @@ seg_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
 }
 
 #ifndef QTNG_SEG4_MINB
-#define QTNG_SEG4_MINB 20  // resident seg4_kernel warps per SM the register budget must allow (96 regs; measured: 16 -> 2.206, 20 -> 2.151, 24 -> 2.149 ms)
+// resident seg4_kernel warps per SM the register budget must allow.  ASAP
+// levels: 16 -> 2.206, 20 (96 regs) -> 2.151, 24 -> 2.149 ms; ALAP levels
+// (bigger quad levels): 16 -> 1.897, 20 -> 1.873, 24 (80 regs) -> 1.862,
+// 28 -> 1.934 ms (two interleaved passes each)
+#define QTNG_SEG4_MINB 24
 #endif
 __global__ void __launch_bounds__(32, QTNG_SEG4_MINB)
 seg4_kernel(const DevSeg* __restrict__ segs, const uint32_t* __restrict__ ibeg,
