@@ -58,12 +58,16 @@ class Pool {
 
  private:
   // Threads (caller included) = QTNG_POOL_THREADS if set, else the hardware
-  // threads minus two on hosts with >= 8 (the caller's process keeps other
-  // threads busy; measured one-shot C2 energy on 16 threads: 16 -> 3.44 ms,
-  // 14 -> 3.41, 12 -> 3.47, 8 -> 3.54).
+  // threads minus four on hosts with >= 12 (minus two with >= 8): the
+  // caller's process keeps other threads busy and the one-shot energy's
+  // enqueue thread (Worker) runs beside the planner.  Measured one-shot C2
+  // energy on 16 threads, medians of 3 runs: 16 -> 3.09-3.25 ms, 14 ->
+  // 3.06-3.11, 12 -> 3.02-3.06, 8 -> 3.11-3.16 (before the enqueue thread:
+  // 14 was best).
   Pool() {
     int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-    if (hw >= 8) hw -= 2;
+    if (hw >= 12) hw -= 4;
+    else if (hw >= 8) hw -= 2;
     if (const char* v = std::getenv("QTNG_POOL_THREADS")) hw = std::max(1, std::atoi(v));
     for (int t = 0; t < std::min(hw, 64) - 1; ++t) workers_.emplace_back([this] { loop(); });
   }
