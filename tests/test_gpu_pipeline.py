@@ -58,3 +58,35 @@ def test_pipeline_chunks_bitwise(golden, env):
         assert r["terms"] == ref
         assert r["energy"] == c["energy_naive"]
         assert r["n_records"] == c["n_records"]
+
+
+@pytest.mark.gpu
+def test_pipeline_shared_context_threads(q, golden):
+    # several host threads on ONE context: the context lock serialises the
+    # device phase (the enqueue thread works for the lock holder); every call
+    # returns the reference's terms
+    import threading
+    c = golden["configs"]["C2"]
+    ref = np.array([complex(x, y) for x, y in c["terms_naive"]])
+    g = q.random_regular(c["n"], 3, c["seed"])
+    a = q.Angles(c["gammas"], c["betas"])
+    ctx = q.Context(0)
+    results, errors = [], []
+
+    def work():
+        try:
+            for _ in range(3):
+                results.append(q.energy_expectation(g, a, q.GpuBackend(ctx)))
+        except Exception as ex:  # reported below
+            errors.append(ex)
+
+    th = [threading.Thread(target=work) for _ in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    assert len(results) == 12
+    for r in results:
+        assert np.array_equal(r.terms, ref)
+        assert r.energy == c["energy_naive"]
